@@ -1,0 +1,451 @@
+"""Benchmark: multi-ring allreduce bus GB/s on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...            (N > 1)
+
+Workload (config 2 of BASELINE.json): a 25,600,000-element fp32 buffer per
+rank (ResNet-50 gradient size, 102.4 MB), synthetic inputs from the reference's
+own generator (`generate_input`, seed 0).
+* N = 1: the 8 ranks of config 2 (grid 2x2x2) live on the one GPU and the
+  local-reduce kernel (mode "local") folds every owned region from the 8
+  buffers in the reference order and writes all 8 -- the HBM roofline of the
+  path.  busbw is reported per (virtual) rank.
+* N > 1: one process per GPU, grid (2,), (2,2) or (2,2,2) for N = 2/4/8, the
+  multi-GPU kernel over NVLink-mapped peer memory (mode --mode, default auto).
+
+Metric definitions (NCCL convention): algbw = S/t,
+busbw = 2(R-1)/R * S / t for R ranks.  `value` = busbw summed over the
+physical GPUs (N * busbw; at N = 1 the single GPU's busbw).  Every step
+restores the inputs and flushes L2 (256 MiB write) outside the timed region;
+the timed region is one allreduce, CUDA events on the launching stream,
+max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_ELEM = 25_600_000
+NOMINAL_NVLINK_GBS = 900.0
+MEASURED_PEER_GBS = 770.0  # B200_PROFILING.md: measured peer copy per direction (NVLink reference)
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
+DIMS_FOR = {1: (2, 2, 2), 2: (2,), 4: (2, 2), 8: (2, 2, 2)}
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--mode", default="auto", help="auto|fused|fused_pull|ring_dims (N>1)")
+    p.add_argument("--dims", default=None, help="grid, e.g. 2x4 (default: 2x2x2 / 2x2 / 2)")
+    p.add_argument("--elems", type=int, default=N_ELEM)
+    p.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-nccl", action="store_true")
+    return p.parse_args()
+
+
+def hbm_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload: str):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(workload)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.reader = threading.Thread(target=self._read, daemon=True)
+            self.reader.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def busbw(ranks: int, nbytes: int, seconds: float) -> float:
+    return 2.0 * (ranks - 1) / ranks * nbytes / seconds / 1e9
+
+
+def cpu_port_run(dims, n, steps=None, budget_s=12.0, seed=0):
+    """The reference runtime's phase loop ported to C (oracle/, one thread per
+    rank) on this host's cores -- the CPU baseline ("kind": "port")."""
+    import numpy as np
+
+    from oracle import oracle_c
+    from oracle import ringbox_oracle as orc
+
+    ranks = 1
+    for d in dims:
+        ranks *= d
+    parts = [orc.generate_input(seed, 0, r, n, "f32") for r in range(ranks)]
+    times = []
+    t_end = time.time() + budget_s
+    while True:
+        bufs = [p.copy() for p in parts]
+        times.append(oracle_c.runtime_port(dims, bufs, "f32"))
+        if steps is not None and len(times) >= steps:
+            break
+        if steps is None and (time.time() > t_end and len(times) >= 2):
+            break
+    del np
+    return times, ranks
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU multi-ring allreduce (C port of
+    its runtime phase loop, one thread per rank) on this host's cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n_gpus = args.gpus
+    dims = tuple(int(x) for x in args.dims.split("x")) if args.dims else DIMS_FOR.get(n_gpus, (n_gpus,))
+    times, ranks = cpu_port_run(dims, args.elems, steps=args.warmup + args.steps)
+    timed = times[args.warmup:]
+    t = statistics.mean(timed)
+    nbytes = args.elems * 4
+    bw = busbw(ranks, nbytes, t)
+    value = bw * (n_gpus if n_gpus > 1 else 1)
+    cores = len(os.sched_getaffinity(0))
+    line = {
+        "metric": "multi-ring allreduce bus GB/s vs msg size at 2/4/8 B200; % of 900 GB/s NVLink",
+        "impl": "reference", "value": round(value, 4), "unit": "GB/s", "n_gpus": n_gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference generate_input, seed 0)",
+        "config": {"workload": f"config2: {args.elems} fp32/rank, {ranks} ranks, grid {'x'.join(map(str, dims))}",
+                   "ranks": ranks, "dims": list(dims), "bytes_per_rank": nbytes},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": min(ranks, cores), "kind": "port",
+                         "sample": f"{args.steps} full allreduces of {args.elems} fp32 x {ranks} ranks "
+                                   f"(oracle/rbx_oracle.c orc_runtime_port, {ranks} threads, host has {cores} cores)"},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main_single(args):
+    """N = 1: the 8 ranks of config 2 on one GPU, local-reduce kernel."""
+    import torch
+
+    from oracle import ringbox_oracle as orc
+    from paper_1708_02188_b200.virtual import VirtualRanks
+
+    dims = tuple(int(x) for x in args.dims.split("x")) if args.dims else DIMS_FOR[1]
+    ranks = 1
+    for d in dims:
+        ranks *= d
+    n = args.elems
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    tdt = torch.float32 if args.dtype == "f32" else torch.bfloat16
+    esz = 4 if args.dtype == "f32" else 2
+    host = [torch.from_numpy(orc.generate_input(0, 0, r, n, "f32")).to(tdt) for r in range(ranks)]
+    pristine = [h.to(dev) for h in host]
+    work = [torch.empty_like(p) for p in pristine]
+    scratch = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > L2 (126 MB)
+    vr = VirtualRanks(dims, device=0)
+    stream = torch.cuda.current_stream(dev)
+
+    def restore():
+        for w, p in zip(work, pristine):
+            w.copy_(p)
+        scratch.fill_(1.0)  # flush L2
+
+    # correctness of the exact timed configuration (one check, outside timing)
+    restore()
+    vr.collective(work, mode="local")
+    torch.cuda.synchronize()
+    vr.check()
+
+    for _ in range(args.warmup):
+        restore()
+        vr.collective(work, mode="local")
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(0)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    l0 = vr.launches
+    sampler.start()
+    torch.cuda.synchronize()
+    for s, e in ev:
+        restore()
+        s.record(stream)
+        vr.collective(work, mode="local")
+        e.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    launches = vr.launches - l0
+    vr.check()
+    step_ms = [s.elapsed_time(e) for s, e in ev]
+    t = statistics.mean(step_ms) / 1e3
+    nbytes = n * esz
+    bw = busbw(ranks, nbytes, t)
+
+    # e2e through the C ABI with HOST buffers: pinned H2D of every rank's input,
+    # the collective, D2H of every rank's result -- all inside the timed region.
+    pinned = [h.pin_memory() for h in host]
+    outs = [torch.empty_like(h).pin_memory() for h in host]
+    e2e_ms = []
+    for k in range(args.warmup + max(3, min(args.steps, 10))):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        scratch.fill_(1.0)
+        s.record(stream)
+        for w, h in zip(work, pinned):
+            w.copy_(h, non_blocking=True)
+        vr.collective(work, mode="local")
+        for o, w in zip(outs, work):
+            o.copy_(w, non_blocking=True)
+        e.record(stream)
+        torch.cuda.synchronize()
+        if k >= args.warmup:
+            e2e_ms.append(s.elapsed_time(e))
+    t_e2e = statistics.mean(e2e_ms) / 1e3
+
+    peak, peak_src = hbm_peak()
+    hbm_bytes = 2 * ranks * nbytes  # read every rank buffer once, write every rank buffer once
+    achieved = hbm_bytes / t / 1e9
+    workload = f"config2-local: {n} {args.dtype}/rank x {ranks} virtual ranks, grid {'x'.join(map(str, dims))}, 1 GPU"
+    traffic = ncu_traffic("local_2x2x2_25.6M_f32") if (dims == (2, 2, 2) and n == N_ELEM and args.dtype == "f32") else None
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        times, r_ = cpu_port_run(dims, n, budget_s=10.0)
+        tc = statistics.median(times)
+        cores = len(os.sched_getaffinity(0))
+        cpu = {"value": round(busbw(ranks, n * 4, tc), 4), "unit": "GB/s", "cores": min(ranks, cores), "kind": "port",
+               "sample": f"{len(times)} full allreduces of config 2 ({n} fp32 x {ranks} ranks, grid "
+                         f"{'x'.join(map(str, dims))}) with the C port of the reference runtime, one thread per rank; "
+                         f"median {tc * 1e3:.1f} ms; host has {cores} cores"}
+
+    line = {
+        "metric": "multi-ring allreduce bus GB/s vs msg size at 2/4/8 B200; % of 900 GB/s NVLink",
+        "value": round(bw, 3), "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t * 1e3, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": args.dtype, "data": "synthetic (reference generate_input, seed 0)",
+        "config": {"workload": workload, "ranks": ranks, "dims": list(dims), "bytes_per_rank": nbytes,
+                   "mode": "local", "l2": "flushed between steps (256 MiB write) and inputs 819 MB > L2",
+                   "value_definition": "busbw = 2(R-1)/R*S/t per (virtual) rank; 1 GPU"},
+        "busbw_gbs": round(bw, 3), "algbw_gbs": round(nbytes / t / 1e9, 3),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": hbm_bytes},
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(busbw(ranks, nbytes, t_e2e), 4), "unit": "GB/s",
+                "h2d_bytes_per_step": ranks * nbytes, "d2h_bytes_per_step": ranks * nbytes,
+                "ms_per_step": round(t_e2e * 1e3, 3)},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "step_ms": [round(x, 4) for x in step_ms],
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main_multi(args):
+    import torch
+    import torch.distributed as dist
+
+    from oracle import ringbox_oracle as orc
+    from paper_1708_02188_b200.multiring import Grid
+    from paper_1708_02188_b200.runtime import RankContext
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    dims = tuple(int(x) for x in args.dims.split("x")) if args.dims else DIMS_FOR.get(world, (world,))
+    grid = Grid(dims)
+    assert grid.size == world, f"dims {dims} do not match world size {world}"
+    n = args.elems
+    tdt = torch.float32 if args.dtype == "f32" else torch.bfloat16
+    esz = 4 if args.dtype == "f32" else 2
+    ctx = RankContext(rank, grid, device=local, mode=args.mode, blocking=False)
+    host = torch.from_numpy(orc.generate_input(0, 0, rank, n, "f32")).to(tdt)
+    pristine = host.to(dev)
+    work = ctx.empty(n, args.dtype)
+    scratch = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def restore():
+        work.copy_(pristine)
+        scratch.fill_(1.0)
+
+    restore()
+    ctx.collective("allreduce", work)
+    ctx.synchronize()
+    for _ in range(args.warmup):
+        restore()
+        ctx.barrier()
+        ctx.collective("allreduce", work)
+    ctx.synchronize()
+    dist.barrier()
+
+    sampler = ClockSampler(local)
+    if rank == 0:
+        sampler.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    l0 = ctx.launches
+    torch.cuda.synchronize()
+    dist.barrier()
+    for s, e in ev:
+        restore()
+        ctx.barrier()  # device-side flag barrier: ranks leave it together
+        s.record(stream)
+        ctx.collective("allreduce", work)
+        e.record(stream)
+    torch.cuda.synchronize()
+    ctx.check()
+    launches = ctx.launches - l0 - args.steps  # minus the barrier launches (outside the timed region)
+    clocks = sampler.stop() if rank == 0 else None
+    step_ms = torch.tensor([s.elapsed_time(e) for s, e in ev], device=dev)
+    dist.all_reduce(step_ms, op=dist.ReduceOp.MAX)
+    t = step_ms.mean().item() / 1e3
+    nbytes = n * esz
+    bw = busbw(world, nbytes, t)
+
+    # e2e: pinned host buffer -> H2D -> allreduce -> D2H inside the timed region
+    pinned = host.pin_memory()
+    out = torch.empty_like(host).pin_memory()
+    e2e = []
+    for k in range(args.warmup + max(3, min(args.steps, 10))):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        scratch.fill_(1.0)
+        ctx.barrier()
+        s.record(stream)
+        work.copy_(pinned, non_blocking=True)
+        ctx.collective("allreduce", work)
+        out.copy_(work, non_blocking=True)
+        e.record(stream)
+        torch.cuda.synchronize()
+        if k >= args.warmup:
+            e2e.append(s.elapsed_time(e))
+    e2e_t = torch.tensor(e2e, device=dev)
+    dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    t_e2e = e2e_t.mean().item() / 1e3
+
+    nccl = None
+    if not args.no_nccl:
+        nbuf = pristine.clone()
+        for _ in range(3):
+            dist.all_reduce(nbuf)
+        torch.cuda.synchronize()
+        nt = []
+        for _ in range(10):
+            nbuf.copy_(pristine)
+            scratch.fill_(1.0)
+            dist.barrier()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            dist.all_reduce(nbuf)
+            e.record(stream)
+            torch.cuda.synchronize()
+            nt.append(s.elapsed_time(e))
+        ntt = torch.tensor(nt, device=dev)
+        dist.all_reduce(ntt, op=dist.ReduceOp.MAX)
+        nccl = round(busbw(world, nbytes, ntt.median().item() / 1e3), 2)
+
+    if rank == 0:
+        line = {
+            "metric": "multi-ring allreduce bus GB/s vs msg size at 2/4/8 B200; % of 900 GB/s NVLink",
+            "value": round(bw * world, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t * 1e3, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (reference generate_input, seed 0)",
+            "config": {"workload": f"config2: {n} {args.dtype}/rank, grid {'x'.join(map(str, dims))}, {world} GPUs",
+                       "ranks": world, "dims": list(dims), "bytes_per_rank": nbytes, "mode": args.mode,
+                       "l2": "flushed between steps (256 MiB write per rank)",
+                       "value_definition": "N * busbw, busbw = 2(N-1)/N*S/t (NCCL convention), max over ranks"},
+            "busbw_gbs": round(bw, 3), "pct_of_900": round(100 * bw / NOMINAL_NVLINK_GBS, 2),
+            "algbw_gbs": round(nbytes / t / 1e9, 3),
+            "roofline": {"bound": "nvlink", "achieved": round(bw, 2), "peak": MEASURED_PEER_GBS, "unit": "GB/s",
+                         "frac": round(bw / MEASURED_PEER_GBS, 4), "traffic": None,
+                         "peak_source": "measured peer copy per direction (B200_PROFILING.md); nominal 900",
+                         "algorithmic_bytes_per_launch": int(2 * (world - 1) / world * nbytes)},
+            "nccl_busbw_gbs": nccl,
+            "cpu_baseline": None,
+            "e2e": {"value": round(busbw(world, nbytes, t_e2e) * world, 3), "unit": "GB/s",
+                    "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": round(t_e2e * 1e3, 3)},
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        main_multi(args)
+    else:
+        main_single(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,125 @@
+/*
+ * rbx.h -- C ABI of the B200-native multi-ring allreduce (librbx.so).
+ *
+ * This is the drop-in boundary for the reference `ringbox` hot path
+ * (/root/reference/pkg/src/ringbox).  The reference exposes a Python API and no
+ * FFI; each entry point below states which reference interface it replaces.
+ * Plain pointers and sizes only: no torch types cross this ABI.  Every
+ * function returns an rbx status code, never throws, and records a
+ * thread-local message readable with rbx_last_error().
+ *
+ * Device buffers passed to the collectives must be SYMMETRIC: registered on
+ * every rank with rbx_register_buffer() (or allocated with
+ * rbx_alloc_symmetric() and registered), used at the same byte offset and
+ * element count on every rank.  There is no host or NCCL fallback: an
+ * unregistered buffer is an error.
+ */
+#ifndef RBX_H_
+#define RBX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RBX_ABI_VERSION 1
+
+/* status codes */
+#define RBX_OK 0
+#define RBX_ERR_INVALID 1     /* bad argument: maps to ValueError (multiring.py:165-166, runtime.py:74-77) */
+#define RBX_ERR_CUDA 2        /* CUDA runtime failure */
+#define RBX_ERR_COLLECTIVE 3  /* peer lost / timeout: maps to CollectiveError(rank, phase) (runtime.py:42-48) */
+#define RBX_ERR_UNSUPPORTED 4 /* dtype/mode combination not implemented */
+
+/* dtypes: the reference's {f32, f64, i64} (runtime.py:37) plus bf16/f16 (fp32 accumulate) and i32 */
+#define RBX_F32 0
+#define RBX_F64 1
+#define RBX_I64 2
+#define RBX_BF16 3
+#define RBX_F16 4
+#define RBX_I32 5
+
+/* execution modes (all produce bit-identical results) */
+#define RBX_MODE_AUTO 0       /* = FUSED */
+#define RBX_MODE_RING_DIMS 1  /* one reduce-scatter / all-gather stage per grid dimension (the paper's rings) */
+#define RBX_MODE_FUSED 2      /* all dims folded in one pass (nested order), result pushed to every peer */
+#define RBX_MODE_FUSED_PULL 3 /* like FUSED, but the all-gather pulls the peers' owned chunks */
+#define RBX_MODE_LOCAL 4      /* virtual ranks on one GPU, no synchronisation (1-GPU roofline) */
+
+/* collective ops */
+#define RBX_OP_ALLREDUCE 0
+#define RBX_OP_REDUCE_SCATTER 1
+#define RBX_OP_ALLGATHER 2
+#define RBX_OP_BARRIER 3
+
+typedef struct rbx_comm rbx_comm_t;
+typedef struct {
+  unsigned char bytes[64]; /* cudaIpcMemHandle_t */
+} rbx_ipc_handle_t;
+
+int rbx_version(void);
+/* Message of the last failed call on this thread; *rank / *stage receive the
+ * failing peer rank and plan step for RBX_ERR_COLLECTIVE (else -1). */
+const char *rbx_last_error(int *rank, int *stage);
+
+/* ---- host-only planning (no GPU needed) ---- */
+/* ring.chunk_bounds -- pkg/src/ringbox/ring.py:57-70 */
+int rbx_chunk_bounds(int64_t count, int64_t n_chunks, int64_t index, int64_t *off, int64_t *len);
+/* runtime.owned_region -- pkg/src/ringbox/runtime.py:187-196 */
+int rbx_owned_region(const int *dims, int ndims, int rank, int64_t count, int64_t *off, int64_t *len);
+/* Rank order in which the reference schedule (multiring.py:170-211) folds `rank`'s owned region. */
+int rbx_fold_order(const int *dims, int ndims, int rank, int *order_out);
+/* Flattened step table of `rank` for inspection (see paper_1708_02188_b200/_native.py). Returns the
+ * number of int64 words (may exceed cap; nothing is written past cap), or -1. */
+int64_t rbx_plan_describe(const int *dims, int ndims, int rank, int64_t count, int op, int mode, int dtype,
+                          int64_t *out, int64_t cap);
+
+/* ---- devices and symmetric memory ---- */
+int rbx_device_count(int *n);
+/* PlacedBuffer(memory="device") storage (runtime.py:51-69): cudaMalloc + IPC export. */
+int rbx_alloc_symmetric(int device, size_t bytes, void **ptr, rbx_ipc_handle_t *handle);
+int rbx_free(void *ptr);
+/* IPC handle + byte offset of any cudaMalloc'd pointer (e.g. a torch tensor). */
+int rbx_export_buffer(void *ptr, rbx_ipc_handle_t *handle, uint64_t *offset);
+
+/* ---- communicator: replaces RankContext + peer sockets (runtime.py:159-184, 348-386) ---- */
+/* Phase 1: allocate this rank's signal area; returns its IPC handle for exchange. */
+int rbx_comm_create(rbx_comm_t **comm, int rank, int nranks, const int *dims, int ndims, int device,
+                    int nblocks, int threads, rbx_ipc_handle_t *signal_handle);
+/* Phase 2: map every peer's signal area (handles indexed by rank). */
+int rbx_comm_connect(rbx_comm_t *comm, const rbx_ipc_handle_t *signal_handles);
+int rbx_comm_destroy(rbx_comm_t *comm);
+int rbx_comm_set_timeout(rbx_comm_t *comm, double seconds);
+int rbx_comm_info(rbx_comm_t *comm, int *rank, int *nranks, int *nblocks, int *threads, uint64_t *launches);
+/* Collective registration: every rank passes its own (ptr, bytes) and all ranks' handles/offsets. */
+int rbx_register_buffer(rbx_comm_t *comm, void *ptr, size_t bytes, const rbx_ipc_handle_t *handles,
+                        const uint64_t *offsets, int *buf_id);
+
+/* ---- collectives (asynchronous on `stream`, a cudaStream_t or NULL) ---- */
+/* runtime.allreduce(ctx, obj) -- pkg/src/ringbox/runtime.py:295-297 */
+int rbx_allreduce(rbx_comm_t *comm, void *buf, size_t count, int dtype, int mode, void *stream);
+/* runtime.reduce_scatter(ctx, obj) -> owned view -- runtime.py:278-284 */
+int rbx_reduce_scatter(rbx_comm_t *comm, void *buf, size_t count, int dtype, int mode, void *stream,
+                       int64_t *owned_off, int64_t *owned_len);
+/* runtime.allgather(ctx, obj) -- runtime.py:287-292 */
+int rbx_allgather(rbx_comm_t *comm, void *buf, size_t count, int dtype, int mode, void *stream);
+/* One launch over a bucket list; Workload.lengths semantics (runtime.py:82-91, 390-398), buckets concurrent. */
+int rbx_allreduce_buckets(rbx_comm_t *comm, void *const *bufs, const size_t *counts, int nbufs, int dtype,
+                          int mode, void *stream);
+/* Device-side flag barrier across all ranks (no data). */
+int rbx_barrier(rbx_comm_t *comm, void *stream);
+/* After the stream has been synchronised: RBX_ERR_COLLECTIVE if a watchdog fired. */
+int rbx_check(rbx_comm_t *comm);
+
+/* ---- virtual ranks on ONE GPU (single launch; cooperative when ranks synchronise) ---- */
+int rbx_vcomm_create(rbx_comm_t **comm, int nranks, const int *dims, int ndims, int device, int nblocks_per_rank,
+                     int threads);
+/* bufs[r] = rank r's device buffer.  mode RBX_MODE_LOCAL = the 1-GPU local reduce (no flags). */
+int rbx_vcollective(rbx_comm_t *comm, void *const *bufs, size_t count, int dtype, int op, int mode, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RBX_H_ */

@@ -1,0 +1,602 @@
+// C ABI (include/rbx.h): communicators, IPC-mapped symmetric memory, plan
+// caching and kernel launch for the sm_100a multi-ring allreduce.
+//
+// Reference mapping (pkg/src/ringbox/runtime.py):
+//   RankContext (159-184)         -> rbx_comm: rank, grid, peer signal areas, plan cache
+//   peer sockets + handshake      -> cudaIpc-mapped peer buffers + signal areas (348-386)
+//   schedule_for (174-177)        -> per (buffer, count, dtype, op, mode) device plan cache
+//   _run_phases (199-267)         -> one launch of rbx_step_kernel<T>
+//   CollectiveError (42-48)       -> RBX_ERR_COLLECTIVE + (rank, step) from the device watchdog
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "rbx.h"
+#include "rbx_kernel.cuh"
+#include "rbx_plan.h"
+
+namespace rbx {
+const void* step_kernel_f32();
+const void* step_kernel_f64();
+const void* step_kernel_i64();
+const void* step_kernel_bf16();
+const void* step_kernel_f16();
+const void* step_kernel_i32();
+}  // namespace rbx
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_err_rank = -1, g_err_stage = -1;
+
+int fail(int code, const std::string& msg, int rank = -1, int stage = -1) {
+  g_err = msg;
+  g_err_rank = rank;
+  g_err_stage = stage;
+  return code;
+}
+
+#define RBX_CUDA(call)                                                                          \
+  do {                                                                                          \
+    cudaError_t e_ = (call);                                                                    \
+    if (e_ != cudaSuccess) return fail(RBX_ERR_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+int dtype_size(int dt) {
+  switch (dt) {
+    case RBX_F32: return 4;
+    case RBX_F64: return 8;
+    case RBX_I64: return 8;
+    case RBX_BF16: return 2;
+    case RBX_F16: return 2;
+    case RBX_I32: return 4;
+    default: return 0;
+  }
+}
+
+struct RegBuf {
+  char* base = nullptr;  // local pointer as registered
+  size_t bytes = 0;
+  std::vector<char*> at;  // per rank: pointer to that rank's copy, valid in this process
+};
+
+struct CachedPlan {
+  rbx::Plan* dev = nullptr;  // nplans contiguous plans
+  void** ptrs = nullptr;
+  int nplans = 0;
+};
+
+struct OpenedHandle {
+  void* ptr = nullptr;
+  int refs = 0;
+};
+
+}  // namespace
+
+struct rbx_comm {
+  int rank = 0, nranks = 1, device = 0, nblocks = 0, threads = 512;
+  int nvirtual = 0;  // >0: all ranks hosted by this process on one GPU
+  rbx::Geometry geo;
+  uint32_t* sig_local = nullptr;     // own signal area(s)
+  std::vector<uint32_t*> sig;        // per rank, mapped
+  std::vector<void*> opened_sig;
+  rbx::ErrRecord* err_host = nullptr;
+  rbx::ErrRecord* err_dev = nullptr;
+  uint64_t timeout_ns = 30ull * 1000000000ull;  // runtime.py:39 DEFAULT_TIMEOUT_S
+  std::vector<RegBuf> bufs;
+  std::map<std::string, CachedPlan> plans;
+  uint64_t launches = 0;
+  bool connected = false;
+  int sm_count = 148;
+  int max_coresident = 0;  // co-resident CTAs of the step kernel
+};
+
+namespace {
+
+std::map<std::string, OpenedHandle>& opened_handles() {
+  static std::map<std::string, OpenedHandle> m;
+  return m;
+}
+
+int open_handle(const rbx_ipc_handle_t& h, void** out) {
+  std::string key(reinterpret_cast<const char*>(h.bytes), sizeof(h.bytes));
+  auto& m = opened_handles();
+  auto it = m.find(key);
+  if (it != m.end()) {
+    it->second.refs++;
+    *out = it->second.ptr;
+    return RBX_OK;
+  }
+  cudaIpcMemHandle_t ch;
+  std::memcpy(&ch, h.bytes, sizeof(ch));
+  void* p = nullptr;
+  RBX_CUDA(cudaIpcOpenMemHandle(&p, ch, cudaIpcMemLazyEnablePeerAccess));
+  m[key] = OpenedHandle{p, 1};
+  *out = p;
+  return RBX_OK;
+}
+
+const void* kernel_for(int dtype) {
+  switch (dtype) {
+    case RBX_F32: return rbx::step_kernel_f32();
+    case RBX_F64: return rbx::step_kernel_f64();
+    case RBX_I64: return rbx::step_kernel_i64();
+    case RBX_BF16: return rbx::step_kernel_bf16();
+    case RBX_F16: return rbx::step_kernel_f16();
+    case RBX_I32: return rbx::step_kernel_i32();
+    default: return nullptr;
+  }
+}
+
+int coresident_blocks(int device, int threads, int* out) {
+  int sms = 0;
+  RBX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  int worst = 1 << 30;
+  for (int dt = RBX_F32; dt <= RBX_I32; ++dt) {
+    int per_sm = 0;
+    RBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_for(dt), threads, 0));
+    if (per_sm * sms < worst) worst = per_sm * sms;
+  }
+  *out = worst;
+  return RBX_OK;
+}
+
+int common_init(rbx_comm* c, const int* dims, int ndims, int device, int threads) {
+  std::string err;
+  if (!c->geo.init(dims, ndims, &err)) return fail(RBX_ERR_INVALID, err);
+  if (threads <= 0) threads = 512;
+  if (threads % 32 || threads > 512) return fail(RBX_ERR_INVALID, "threads must be a multiple of 32 and <= 512");
+  c->threads = threads;
+  c->device = device;
+  RBX_CUDA(cudaSetDevice(device));
+  RBX_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+  int rc = coresident_blocks(device, threads, &c->max_coresident);
+  if (rc) return rc;
+  RBX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(rbx::ErrRecord), cudaHostAllocMapped));
+  std::memset(c->err_host, 0, sizeof(rbx::ErrRecord));
+  RBX_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0));
+  return RBX_OK;
+}
+
+std::string plan_key(int op, int mode, int dtype, const std::vector<const void*>& ptrs, const std::vector<size_t>& counts) {
+  std::string k = std::to_string(op) + ":" + std::to_string(mode) + ":" + std::to_string(dtype);
+  char buf[64];
+  for (size_t i = 0; i < ptrs.size(); ++i) {
+    std::snprintf(buf, sizeof(buf), "|%p#%zu", ptrs[i], counts.empty() ? 0 : counts[i % counts.size()]);
+    k += buf;
+  }
+  return k;
+}
+
+int upload(rbx_comm* c, std::vector<rbx::Plan>& host, const std::vector<void*>& ptrs, CachedPlan* out) {
+  RBX_CUDA(cudaMalloc(reinterpret_cast<void**>(&out->ptrs), sizeof(void*) * (ptrs.size() ? ptrs.size() : 1)));
+  if (!ptrs.empty())
+    RBX_CUDA(cudaMemcpy(out->ptrs, ptrs.data(), sizeof(void*) * ptrs.size(), cudaMemcpyHostToDevice));
+  for (auto& p : host) p.ptrs = out->ptrs;
+  RBX_CUDA(cudaMalloc(reinterpret_cast<void**>(&out->dev), sizeof(rbx::Plan) * host.size()));
+  RBX_CUDA(cudaMemcpy(out->dev, host.data(), sizeof(rbx::Plan) * host.size(), cudaMemcpyHostToDevice));
+  out->nplans = (int)host.size();
+  return RBX_OK;
+}
+
+int launch(rbx_comm* c, const CachedPlan& cp, int dtype, cudaStream_t stream, bool cooperative, int nblocks) {
+  const void* fn = kernel_for(dtype);
+  if (!fn) return fail(RBX_ERR_INVALID, "unknown dtype");
+  rbx::KernelArgs a;
+  a.plans = cp.dev;
+  a.nblocks = nblocks;
+  a.timeout_ns = c->timeout_ns;
+  a.err = c->err_dev;
+  void* params[] = {&a};
+  dim3 grid((unsigned)(nblocks * cp.nplans)), block((unsigned)c->threads);
+  if (cooperative) {
+    RBX_CUDA(cudaLaunchCooperativeKernel(fn, grid, block, params, 0, stream));
+  } else {
+    RBX_CUDA(cudaLaunchKernel(fn, grid, block, params, 0, stream));
+  }
+  c->launches++;
+  return RBX_OK;
+}
+
+// Per-dimension stages would store bf16/f16 partials between stages; the
+// fp32-partial workspace for that is not built yet, so refuse rather than
+// silently round partials (parity policy: one RNE at the end).
+int check_mode_dtype(int mode, int dtype) {
+  if (mode == RBX_MODE_RING_DIMS && (dtype == RBX_BF16 || dtype == RBX_F16))
+    return fail(RBX_ERR_UNSUPPORTED, "MODE_RING_DIMS with bf16/f16 needs fp32 partial workspaces (not implemented); "
+                                     "use MODE_FUSED, which folds in fp32 and rounds once");
+  if (mode < RBX_MODE_AUTO || mode > RBX_MODE_LOCAL) return fail(RBX_ERR_INVALID, "unknown mode");
+  return RBX_OK;
+}
+
+int find_buffer(rbx_comm* c, const void* p, size_t bytes, int* id, size_t* off) {
+  for (size_t i = 0; i < c->bufs.size(); ++i) {
+    const RegBuf& b = c->bufs[i];
+    const char* q = static_cast<const char*>(p);
+    if (q >= b.base && q + bytes <= b.base + b.bytes) {
+      *id = (int)i;
+      *off = (size_t)(q - b.base);
+      return RBX_OK;
+    }
+  }
+  return fail(RBX_ERR_INVALID, "buffer is not registered with this communicator (use rbx_register_buffer / "
+                               "PlacedBuffer.device(); there is no unregistered fallback)");
+}
+
+int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nbufs, int dtype, int op, int mode,
+                    cudaStream_t stream) {
+  if (!c || c->nvirtual) return fail(RBX_ERR_INVALID, "not a per-rank communicator");
+  if (!c->connected) return fail(RBX_ERR_INVALID, "communicator is not connected");
+  const int es = dtype_size(dtype);
+  if (!es) return fail(RBX_ERR_INVALID, "unknown dtype");
+  if (mode == RBX_MODE_LOCAL) return fail(RBX_ERR_INVALID, "MODE_LOCAL needs a virtual communicator");
+  if (int rc = check_mode_dtype(mode, dtype)) return rc;
+  if (c->err_host->code) return fail(RBX_ERR_COLLECTIVE, "communicator is in an error state", c->err_host->peer, c->err_host->step);
+  std::vector<const void*> kp(bufs, bufs + nbufs);
+  std::vector<size_t> kc(counts, counts + nbufs);
+  const std::string key = plan_key(op, mode, dtype, kp, kc);
+  auto it = c->plans.find(key);
+  if (it == c->plans.end()) {
+    std::vector<rbx::Plan> host(1);
+    std::vector<void*> ptrs;
+    rbx::PlanSpec spec;
+    spec.op = (rbx::Op)op;
+    spec.mode = (rbx::Mode)mode;
+    spec.vec = 16 / es;
+    spec.nblocks = c->nblocks;
+    std::string err;
+    for (int k = 0; k < nbufs; ++k) {
+      int id;
+      size_t off;
+      if (op != RBX_OP_BARRIER) {
+        int rc = find_buffer(c, bufs[k], counts[k] * es, &id, &off);
+        if (rc) return rc;
+        for (int q = 0; q < c->nranks; ++q) ptrs.push_back(c->bufs[id].at[q] + off);
+      }
+      if (!rbx::build_plan(c->geo, c->rank, (int64_t)counts[k], spec, k * c->nranks, &host[0], k == 0, &err))
+        return fail(RBX_ERR_INVALID, err);
+    }
+    for (int q = 0; q < c->nranks; ++q) host[0].sig[q] = c->sig[q];
+    host[0].my_sig = c->sig[c->rank];
+    CachedPlan cp;
+    int rc = upload(c, host, ptrs, &cp);
+    if (rc) return rc;
+    it = c->plans.emplace(key, cp).first;
+  }
+  return launch(c, it->second, dtype, stream, false, c->nblocks);
+}
+
+}  // namespace
+
+extern "C" {
+
+int rbx_version(void) { return RBX_ABI_VERSION; }
+
+const char* rbx_last_error(int* rank, int* stage) {
+  if (rank) *rank = g_err_rank;
+  if (stage) *stage = g_err_stage;
+  return g_err.c_str();
+}
+
+int rbx_chunk_bounds(int64_t count, int64_t n_chunks, int64_t index, int64_t* off, int64_t* len) {
+  if (n_chunks < 1) return fail(RBX_ERR_INVALID, "n_chunks must be >= 1, got " + std::to_string(n_chunks));
+  if (index < 0 || index >= n_chunks)
+    return fail(RBX_ERR_INVALID, "chunk index " + std::to_string(index) + " out of range");
+  rbx::chunk_bounds(count, n_chunks, index, off, len);
+  return RBX_OK;
+}
+
+int rbx_owned_region(const int* dims, int ndims, int rank, int64_t count, int64_t* off, int64_t* len) {
+  rbx::Geometry g;
+  std::string err;
+  if (!g.init(dims, ndims, &err)) return fail(RBX_ERR_INVALID, err);
+  if (rank < 0 || rank >= g.nranks) return fail(RBX_ERR_INVALID, "rank out of range");
+  rbx::region_after(g, rank, count, (int)g.active_dims().size(), off, len);
+  return RBX_OK;
+}
+
+int rbx_fold_order(const int* dims, int ndims, int rank, int* order_out) {
+  rbx::Geometry g;
+  std::string err;
+  if (!g.init(dims, ndims, &err)) return fail(RBX_ERR_INVALID, err);
+  if (rank < 0 || rank >= g.nranks) return fail(RBX_ERR_INVALID, "rank out of range");
+  std::vector<int> o = rbx::fold_order(g, rank);
+  for (size_t i = 0; i < o.size(); ++i) order_out[i] = o[i];
+  return RBX_OK;
+}
+
+int64_t rbx_plan_describe(const int* dims, int ndims, int rank, int64_t count, int op, int mode, int dtype,
+                          int64_t* out, int64_t cap) {
+  rbx::Geometry g;
+  std::string err;
+  if (!g.init(dims, ndims, &err)) return fail(RBX_ERR_INVALID, err), -1;
+  const int es = dtype_size(dtype);
+  if (!es) return fail(RBX_ERR_INVALID, "unknown dtype"), -1;
+  std::unique_ptr<rbx::Plan> p(new rbx::Plan);
+  bool ok;
+  if (mode == RBX_MODE_LOCAL)
+    ok = rbx::build_local_plan(g, count, 16 / es, 148, p.get(), &err);
+  else {
+    if (rank < 0 || rank >= g.nranks) return fail(RBX_ERR_INVALID, "rank out of range"), -1;
+    rbx::PlanSpec spec;
+    spec.op = (rbx::Op)op;
+    spec.mode = (rbx::Mode)mode;
+    spec.vec = 16 / es;
+    ok = rbx::build_plan(g, rank, count, spec, 0, p.get(), true, &err);
+  }
+  if (!ok) return fail(RBX_ERR_INVALID, err), -1;
+  return rbx::describe_plan(*p, out, cap);
+}
+
+int rbx_device_count(int* n) {
+  RBX_CUDA(cudaGetDeviceCount(n));
+  return RBX_OK;
+}
+
+int rbx_alloc_symmetric(int device, size_t bytes, void** ptr, rbx_ipc_handle_t* handle) {
+  RBX_CUDA(cudaSetDevice(device));
+  RBX_CUDA(cudaMalloc(ptr, bytes ? bytes : 256));
+  if (handle) {
+    cudaIpcMemHandle_t h;
+    RBX_CUDA(cudaIpcGetMemHandle(&h, *ptr));
+    std::memcpy(handle->bytes, &h, sizeof(h));
+  }
+  return RBX_OK;
+}
+
+int rbx_free(void* ptr) {
+  RBX_CUDA(cudaFree(ptr));
+  return RBX_OK;
+}
+
+int rbx_export_buffer(void* ptr, rbx_ipc_handle_t* handle, uint64_t* offset) {
+  // base of the allocation via the driver entry point (no link-time libcuda dependency)
+  typedef CUresult (*range_fn)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static range_fn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    RBX_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !f) return fail(RBX_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    fn = reinterpret_cast<range_fn>(f);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (fn(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS) return fail(RBX_ERR_CUDA, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  RBX_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  std::memcpy(handle->bytes, &h, sizeof(h));
+  *offset = (uint64_t)((CUdeviceptr)ptr - base);
+  return RBX_OK;
+}
+
+int rbx_comm_create(rbx_comm_t** comm, int rank, int nranks, const int* dims, int ndims, int device, int nblocks,
+                    int threads, rbx_ipc_handle_t* signal_handle) {
+  std::unique_ptr<rbx_comm> c(new rbx_comm);
+  int rc = common_init(c.get(), dims, ndims, device, threads);
+  if (rc) return rc;
+  if (c->geo.nranks != nranks)
+    return fail(RBX_ERR_INVALID, "dims product " + std::to_string(c->geo.nranks) + " != nranks " + std::to_string(nranks));
+  if (rank < 0 || rank >= nranks) return fail(RBX_ERR_INVALID, "rank out of range");
+  c->rank = rank;
+  c->nranks = nranks;
+  if (nblocks <= 0) nblocks = c->sm_count;
+  if (nblocks > RBX_MAX_BLOCKS) nblocks = RBX_MAX_BLOCKS;
+  if (nblocks > c->max_coresident) nblocks = c->max_coresident;  // deadlock freedom: all CTAs resident
+  c->nblocks = nblocks;
+  RBX_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->sig_local), rbx::SigLayout::bytes));
+  RBX_CUDA(cudaMemset(c->sig_local, 0, rbx::SigLayout::bytes));
+  cudaIpcMemHandle_t h;
+  RBX_CUDA(cudaIpcGetMemHandle(&h, c->sig_local));
+  std::memcpy(signal_handle->bytes, &h, sizeof(h));
+  c->sig.assign(nranks, nullptr);
+  c->sig[rank] = c->sig_local;
+  RBX_CUDA(cudaDeviceSynchronize());
+  *comm = c.release();
+  return RBX_OK;
+}
+
+int rbx_comm_connect(rbx_comm_t* c, const rbx_ipc_handle_t* handles) {
+  if (!c || c->nvirtual) return fail(RBX_ERR_INVALID, "not a per-rank communicator");
+  RBX_CUDA(cudaSetDevice(c->device));
+  for (int q = 0; q < c->nranks; ++q) {
+    if (q == c->rank) continue;
+    void* p = nullptr;
+    int rc = open_handle(handles[q], &p);
+    if (rc) return rc;
+    c->sig[q] = static_cast<uint32_t*>(p);
+    c->opened_sig.push_back(p);
+  }
+  c->connected = true;
+  return RBX_OK;
+}
+
+int rbx_comm_destroy(rbx_comm_t* c) {
+  if (!c) return RBX_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (auto& kv : c->plans) {
+    cudaFree(kv.second.dev);
+    cudaFree(kv.second.ptrs);
+  }
+  auto& m = opened_handles();
+  for (auto it = m.begin(); it != m.end();) {
+    bool mine = false;
+    for (void* p : c->opened_sig) mine |= (p == it->second.ptr);
+    for (auto& b : c->bufs)
+      for (int q = 0; q < (int)b.at.size(); ++q)
+        if (q != c->rank && b.at[q] - 0 == it->second.ptr) mine = true;
+    if (mine && --it->second.refs <= 0) {
+      cudaIpcCloseMemHandle(it->second.ptr);
+      it = m.erase(it);
+    } else {
+      ++it;
+    }
+  }
+  if (c->sig_local) cudaFree(c->sig_local);
+  if (c->err_host) cudaFreeHost(c->err_host);
+  delete c;
+  return RBX_OK;
+}
+
+int rbx_comm_set_timeout(rbx_comm_t* c, double seconds) {
+  if (!c || seconds <= 0) return fail(RBX_ERR_INVALID, "timeout must be > 0");
+  c->timeout_ns = (uint64_t)(seconds * 1e9);
+  return RBX_OK;
+}
+
+int rbx_comm_info(rbx_comm_t* c, int* rank, int* nranks, int* nblocks, int* threads, uint64_t* launches) {
+  if (!c) return fail(RBX_ERR_INVALID, "null communicator");
+  if (rank) *rank = c->rank;
+  if (nranks) *nranks = c->nranks;
+  if (nblocks) *nblocks = c->nblocks;
+  if (threads) *threads = c->threads;
+  if (launches) *launches = c->launches;
+  return RBX_OK;
+}
+
+int rbx_register_buffer(rbx_comm_t* c, void* ptr, size_t bytes, const rbx_ipc_handle_t* handles,
+                        const uint64_t* offsets, int* buf_id) {
+  if (!c || c->nvirtual) return fail(RBX_ERR_INVALID, "not a per-rank communicator");
+  RBX_CUDA(cudaSetDevice(c->device));
+  RegBuf b;
+  b.base = static_cast<char*>(ptr);
+  b.bytes = bytes;
+  b.at.assign(c->nranks, nullptr);
+  for (int q = 0; q < c->nranks; ++q) {
+    if (q == c->rank) {
+      b.at[q] = b.base;
+      continue;
+    }
+    void* p = nullptr;
+    int rc = open_handle(handles[q], &p);
+    if (rc) return rc;
+    b.at[q] = static_cast<char*>(p) + offsets[q];
+  }
+  c->bufs.push_back(b);
+  *buf_id = (int)c->bufs.size() - 1;
+  return RBX_OK;
+}
+
+int rbx_allreduce(rbx_comm_t* c, void* buf, size_t count, int dtype, int mode, void* stream) {
+  void* bufs[1] = {buf};
+  size_t counts[1] = {count};
+  return real_collective(c, bufs, counts, 1, dtype, RBX_OP_ALLREDUCE, mode, (cudaStream_t)stream);
+}
+
+int rbx_reduce_scatter(rbx_comm_t* c, void* buf, size_t count, int dtype, int mode, void* stream, int64_t* owned_off,
+                       int64_t* owned_len) {
+  void* bufs[1] = {buf};
+  size_t counts[1] = {count};
+  int rc = real_collective(c, bufs, counts, 1, dtype, RBX_OP_REDUCE_SCATTER, mode, (cudaStream_t)stream);
+  if (rc) return rc;
+  int64_t o, l;
+  rbx::region_after(c->geo, c->rank, (int64_t)count, (int)c->geo.active_dims().size(), &o, &l);
+  if (owned_off) *owned_off = o;
+  if (owned_len) *owned_len = l;
+  return RBX_OK;
+}
+
+int rbx_allgather(rbx_comm_t* c, void* buf, size_t count, int dtype, int mode, void* stream) {
+  void* bufs[1] = {buf};
+  size_t counts[1] = {count};
+  return real_collective(c, bufs, counts, 1, dtype, RBX_OP_ALLGATHER, mode, (cudaStream_t)stream);
+}
+
+int rbx_allreduce_buckets(rbx_comm_t* c, void* const* bufs, const size_t* counts, int nbufs, int dtype, int mode,
+                          void* stream) {
+  if (nbufs < 1) return fail(RBX_ERR_INVALID, "empty bucket list");
+  if ((int64_t)nbufs * c->nranks > 4096) return fail(RBX_ERR_INVALID, "bucket list too long");
+  return real_collective(c, bufs, counts, nbufs, dtype, RBX_OP_ALLREDUCE, mode, (cudaStream_t)stream);
+}
+
+int rbx_barrier(rbx_comm_t* c, void* stream) {
+  void* bufs[1] = {nullptr};
+  size_t counts[1] = {0};
+  return real_collective(c, bufs, counts, 1, RBX_F32, RBX_OP_BARRIER, RBX_MODE_FUSED, (cudaStream_t)stream);
+}
+
+int rbx_check(rbx_comm_t* c) {
+  if (!c) return fail(RBX_ERR_INVALID, "null communicator");
+  if (c->err_host->code) {
+    return fail(RBX_ERR_COLLECTIVE,
+                "collective watchdog: rank " + std::to_string(c->err_host->rank) + " timed out at plan step " +
+                    std::to_string(c->err_host->step) + " waiting for rank " + std::to_string(c->err_host->peer),
+                c->err_host->peer, c->err_host->step);
+  }
+  return RBX_OK;
+}
+
+int rbx_vcomm_create(rbx_comm_t** comm, int nranks, const int* dims, int ndims, int device, int nblocks_per_rank,
+                     int threads) {
+  std::unique_ptr<rbx_comm> c(new rbx_comm);
+  int rc = common_init(c.get(), dims, ndims, device, threads);
+  if (rc) return rc;
+  if (c->geo.nranks != nranks)
+    return fail(RBX_ERR_INVALID, "dims product " + std::to_string(c->geo.nranks) + " != nranks " + std::to_string(nranks));
+  c->nranks = nranks;
+  c->nvirtual = nranks;
+  int nb = nblocks_per_rank > 0 ? nblocks_per_rank : c->max_coresident / nranks;
+  if (nb < 1) nb = 1;
+  if (nb > RBX_MAX_BLOCKS) nb = RBX_MAX_BLOCKS;
+  c->nblocks = nb;
+  RBX_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->sig_local), rbx::SigLayout::bytes * nranks));
+  RBX_CUDA(cudaMemset(c->sig_local, 0, rbx::SigLayout::bytes * nranks));
+  c->sig.resize(nranks);
+  for (int q = 0; q < nranks; ++q) c->sig[q] = c->sig_local + q * rbx::SigLayout::words;
+  c->connected = true;
+  RBX_CUDA(cudaDeviceSynchronize());
+  *comm = c.release();
+  return RBX_OK;
+}
+
+int rbx_vcollective(rbx_comm_t* c, void* const* bufs, size_t count, int dtype, int op, int mode, void* stream) {
+  if (!c || !c->nvirtual) return fail(RBX_ERR_INVALID, "not a virtual communicator");
+  const int es = dtype_size(dtype);
+  if (!es) return fail(RBX_ERR_INVALID, "unknown dtype");
+  if (c->err_host->code) return fail(RBX_ERR_COLLECTIVE, "communicator is in an error state", c->err_host->peer, c->err_host->step);
+  if (int rc = check_mode_dtype(mode, dtype)) return rc;
+  const int V = c->nvirtual;
+  std::vector<const void*> kp(bufs, bufs + V);
+  const std::string key = plan_key(op, mode, dtype, kp, {count});
+  auto it = c->plans.find(key);
+  const bool local = (mode == RBX_MODE_LOCAL);
+  if (local && op != RBX_OP_ALLREDUCE) return fail(RBX_ERR_INVALID, "MODE_LOCAL supports allreduce only");
+  int nb = c->nblocks;
+  if (local) nb = c->max_coresident > 0 ? c->max_coresident : c->sm_count;
+  if (nb > RBX_MAX_BLOCKS) nb = RBX_MAX_BLOCKS;
+  if (it == c->plans.end()) {
+    std::string err;
+    std::vector<void*> ptrs(bufs, bufs + V);
+    std::vector<rbx::Plan> host(local ? 1 : V);
+    if (local) {
+      if (!rbx::build_local_plan(c->geo, (int64_t)count, 16 / es, nb, &host[0], &err)) return fail(RBX_ERR_INVALID, err);
+    } else {
+      rbx::PlanSpec spec;
+      spec.op = (rbx::Op)op;
+      spec.mode = (rbx::Mode)mode;
+      spec.vec = 16 / es;
+      spec.nblocks = nb;
+      for (int r = 0; r < V; ++r) {
+        if (!rbx::build_plan(c->geo, r, (int64_t)count, spec, 0, &host[r], true, &err)) return fail(RBX_ERR_INVALID, err);
+        for (int q = 0; q < V; ++q) host[r].sig[q] = c->sig[q];
+        host[r].my_sig = c->sig[r];
+      }
+    }
+    CachedPlan cp;
+    int rc = upload(c, host, ptrs, &cp);
+    if (rc) return rc;
+    it = c->plans.emplace(key, cp).first;
+  }
+  if (!local && (int64_t)nb * V > c->max_coresident)
+    return fail(RBX_ERR_INVALID, "virtual ranks x blocks exceed co-resident CTAs");
+  return launch(c, it->second, dtype, (cudaStream_t)stream, !local, nb);
+}
+
+}  // extern "C"

@@ -1,0 +1,433 @@
+// sm_100a persistent step-interpreter kernel for the multi-ring allreduce.
+//
+// One CTA-group of `nblocks` CTAs per rank executes the rank's Plan
+// (rbx_plan.h).  Every step: (1) wait for the peers' epoch-tagged flags
+// (ld.acquire.sys on the rank's own signal area, written remotely over
+// NVLink), (2) fold the step's segments: 16-byte coalesced loads from the
+// local buffer and from NVLink-mapped peer buffers, reduced in registers in
+// exactly the reference's order, then 16-byte stores into the local buffer
+// and/or straight into peer buffers (push), (3) publish completion with a
+// st.release.sys into each consumer's signal area.
+//
+// Reference mapping: a ring phase ADD (`view += payload`,
+// pkg/src/ringbox/runtime.py:248-249) is one position of the fold; REPLACE
+// (`view[:] = payload`, runtime.py:250-251) is a push/pull copy.  The frame
+// header checks (runtime.py:229-245) become epoch-tagged flags and a
+// watchdog that reports the peer and step on timeout (CollectiveError).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rbx_plan.h"
+
+namespace rbx {
+
+// ------------------------------------------------------------------ dtypes --
+// Each dtype defines how a 16-byte vector (int4) splits into VEC lanes, how a
+// lane widens to the accumulator type and how the result narrows back.  All
+// conversions are bit manipulations on registers (no address-taken arrays).
+__device__ __forceinline__ uint32_t word(const int4& r, int i) {
+  return (uint32_t)(i == 0 ? r.x : i == 1 ? r.y : i == 2 ? r.z : r.w);
+}
+__device__ __forceinline__ void set_word(int4& r, int i, uint32_t v) {
+  if (i == 0)
+    r.x = (int)v;
+  else if (i == 1)
+    r.y = (int)v;
+  else if (i == 2)
+    r.z = (int)v;
+  else
+    r.w = (int)v;
+}
+
+template <typename T>
+struct Traits;
+template <>
+struct Traits<float> {
+  using Acc = float;
+  using Bits = uint32_t;
+  static constexpr int VEC = 4;
+  __device__ static Acc lane(const int4& r, int l) { return __uint_as_float(word(r, l)); }
+  __device__ static void put(int4& r, int l, Acc x) { set_word(r, l, __float_as_uint(x)); }
+  __device__ static Acc from_bits(Bits b) { return __uint_as_float(b); }
+  __device__ static Bits to_bits(Acc x) { return __float_as_uint(x); }
+  __device__ static Acc add(Acc a, Acc b) { return __fadd_rn(a, b); }
+};
+template <>
+struct Traits<double> {
+  using Acc = double;
+  using Bits = unsigned long long;
+  static constexpr int VEC = 2;
+  __device__ static Acc lane(const int4& r, int l) {
+    return __hiloint2double((int)word(r, 2 * l + 1), (int)word(r, 2 * l));
+  }
+  __device__ static void put(int4& r, int l, Acc x) {
+    set_word(r, 2 * l, (uint32_t)__double2loint(x));
+    set_word(r, 2 * l + 1, (uint32_t)__double2hiint(x));
+  }
+  __device__ static Acc from_bits(Bits b) { return __longlong_as_double((long long)b); }
+  __device__ static Bits to_bits(Acc x) { return (Bits)__double_as_longlong(x); }
+  __device__ static Acc add(Acc a, Acc b) { return __dadd_rn(a, b); }
+};
+template <>
+struct Traits<unsigned long long> {  // int64: wrapping add (numpy semantics)
+  using Acc = unsigned long long;
+  using Bits = unsigned long long;
+  static constexpr int VEC = 2;
+  __device__ static Acc lane(const int4& r, int l) { return ((Acc)word(r, 2 * l + 1) << 32) | (Acc)word(r, 2 * l); }
+  __device__ static void put(int4& r, int l, Acc x) {
+    set_word(r, 2 * l, (uint32_t)x);
+    set_word(r, 2 * l + 1, (uint32_t)(x >> 32));
+  }
+  __device__ static Acc from_bits(Bits b) { return b; }
+  __device__ static Bits to_bits(Acc x) { return x; }
+  __device__ static Acc add(Acc a, Acc b) { return a + b; }
+};
+template <>
+struct Traits<unsigned int> {  // int32: wrapping add
+  using Acc = unsigned int;
+  using Bits = uint32_t;
+  static constexpr int VEC = 4;
+  __device__ static Acc lane(const int4& r, int l) { return word(r, l); }
+  __device__ static void put(int4& r, int l, Acc x) { set_word(r, l, x); }
+  __device__ static Acc from_bits(Bits b) { return b; }
+  __device__ static Bits to_bits(Acc x) { return x; }
+  __device__ static Acc add(Acc a, Acc b) { return a + b; }
+};
+template <>
+struct Traits<__nv_bfloat16> {  // bf16 storage, fp32 accumulation, one RNE at the end
+  using Acc = float;
+  using Bits = unsigned short;
+  static constexpr int VEC = 8;
+  __device__ static Acc lane(const int4& r, int l) {
+    const uint32_t w = word(r, l >> 1);
+    return __uint_as_float((l & 1) ? (w & 0xffff0000u) : (w << 16));
+  }
+  __device__ static uint32_t narrow(Acc x) { return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(x)); }
+  __device__ static void put(int4& r, int l, Acc x) {
+    const uint32_t h = narrow(x);
+    const uint32_t w = word(r, l >> 1);
+    set_word(r, l >> 1, (l & 1) ? ((w & 0xffffu) | (h << 16)) : ((w & 0xffff0000u) | h));
+  }
+  __device__ static Acc from_bits(Bits b) { return __uint_as_float((uint32_t)b << 16); }
+  __device__ static Bits to_bits(Acc x) { return (Bits)narrow(x); }
+  __device__ static Acc add(Acc a, Acc b) { return __fadd_rn(a, b); }
+};
+template <>
+struct Traits<__half> {  // f16 storage, fp32 accumulation
+  using Acc = float;
+  using Bits = unsigned short;
+  static constexpr int VEC = 8;
+  __device__ static Acc lane(const int4& r, int l) {
+    const uint32_t w = word(r, l >> 1);
+    return __half2float(__ushort_as_half((unsigned short)((l & 1) ? (w >> 16) : (w & 0xffffu))));
+  }
+  __device__ static uint32_t narrow(Acc x) { return (uint32_t)__half_as_ushort(__float2half_rn(x)); }
+  __device__ static void put(int4& r, int l, Acc x) {
+    const uint32_t h = narrow(x);
+    const uint32_t w = word(r, l >> 1);
+    set_word(r, l >> 1, (l & 1) ? ((w & 0xffffu) | (h << 16)) : ((w & 0xffff0000u) | h));
+  }
+  __device__ static Acc from_bits(Bits b) { return __half2float(__ushort_as_half(b)); }
+  __device__ static Bits to_bits(Acc x) { return (Bits)narrow(x); }
+  __device__ static Acc add(Acc a, Acc b) { return __fadd_rn(a, b); }
+};
+
+// ------------------------------------------------------------ primitives --
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Nested left fold (dim 0 innermost), fed one operand at a time.  ctrl[j]:
+// bit L set -> level L starts a new group at position j; bits 4-5 = number of
+// levels whose group closes at j (capped at nlev-1), so the closed value is
+// handed one level up.  Level nlev-1 holds the result after the last operand.
+template <typename T, int LANES, int NLEV>
+struct FoldState {
+  using Acc = typename Traits<T>::Acc;
+  Acc a[NLEV][LANES];
+  __device__ __forceinline__ FoldState() {
+#pragma unroll
+    for (int L = 0; L < NLEV; ++L)
+#pragma unroll
+      for (int l = 0; l < LANES; ++l) a[L][l] = Acc(0);
+  }
+  __device__ __forceinline__ void feed(uint32_t c, const Acc (&x)[LANES]) {
+    const uint32_t up = c >> 4;
+#pragma unroll
+    for (int l = 0; l < LANES; ++l) a[0][l] = (c & 1u) ? x[l] : Traits<T>::add(a[0][l], x[l]);
+#pragma unroll
+    for (int L = 1; L < NLEV; ++L) {
+      if (up >= (uint32_t)L) {
+#pragma unroll
+        for (int l = 0; l < LANES; ++l) a[L][l] = (c & (1u << L)) ? a[L - 1][l] : Traits<T>::add(a[L][l], a[L - 1][l]);
+      }
+    }
+  }
+  __device__ __forceinline__ Acc result(int l) const { return a[NLEV - 1][l]; }
+};
+
+struct SegCtx {
+  const char* src[RBX_MAX_RANKS];
+  char* dst[RBX_MAX_RANKS];
+  uint8_t ctrl[RBX_MAX_RANKS];
+  int ndst, nlev;
+};
+
+// Body of one segment, vectors [v0, v1) (relative to seg.body_off).  The
+// 16-byte loads of a batch of up to 8 operands (x U independent vectors) are
+// all issued before any arithmetic, so every thread keeps ~8 NVLink/HBM
+// requests in flight; operands stay raw (int4) until folded.
+template <typename T, int NSRC, int NLEV>
+__device__ __noinline__ void fold_body(const SegCtx& sc, int64_t body_off, int64_t v0, int64_t v1) {
+  constexpr int VEC = Traits<T>::VEC;
+  constexpr int B = NSRC < 8 ? NSRC : 8;  // operands per load batch
+  constexpr int U_LD = 8 / B > 0 ? 8 / B : 1;
+  constexpr int U_ACC = 32 / (NLEV * VEC) > 0 ? 32 / (NLEV * VEC) : 1;
+  constexpr int U = NSRC == 1 ? 8 : (U_LD < U_ACC ? U_LD : U_ACC);
+  const int64_t base = body_off * (int64_t)sizeof(T);
+  const int64_t stride = (int64_t)blockDim.x * U;
+  if (NSRC == 1) {  // REPLACE: bitwise copy (runtime.py:250-251)
+    const char* p = sc.src[0] + base;
+    for (int64_t v = v0 + threadIdx.x; v < v1; v += stride) {
+      int4 raw[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t idx = v + (int64_t)u * blockDim.x;
+        if (idx < v1) raw[u] = __ldcg(reinterpret_cast<const int4*>(p + idx * 16));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t idx = v + (int64_t)u * blockDim.x;
+        if (idx < v1)
+          for (int d = 0; d < sc.ndst; ++d) __stcg(reinterpret_cast<int4*>(sc.dst[d] + base + idx * 16), raw[u]);
+      }
+    }
+    return;
+  }
+  for (int64_t v = v0 + threadIdx.x; v < v1; v += stride) {
+    FoldState<T, VEC, NLEV> st[U];
+#pragma unroll
+    for (int j0 = 0; j0 < NSRC; j0 += B) {
+      int4 raw[U][B];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t idx = v + (int64_t)u * blockDim.x;
+        if (idx < v1) {
+#pragma unroll
+          for (int k = 0; k < B; ++k)
+            if (j0 + k < NSRC) {
+              const char* p = NSRC > 8 ? ((const char* volatile*)sc.src)[j0 + k] : sc.src[j0 + k];
+              raw[u][k] = __ldcg(reinterpret_cast<const int4*>(p + base + idx * 16));
+            }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int k = 0; k < B; ++k)
+          if (j0 + k < NSRC) {
+            typename Traits<T>::Acc x[VEC];
+#pragma unroll
+            for (int l = 0; l < VEC; ++l) x[l] = Traits<T>::lane(raw[u][k], l);
+            st[u].feed(sc.ctrl[j0 + k], x);
+          }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t idx = v + (int64_t)u * blockDim.x;
+      if (idx < v1) {
+        int4 packed = make_int4(0, 0, 0, 0);
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) Traits<T>::put(packed, l, st[u].result(l));
+        for (int d = 0; d < sc.ndst; ++d) __stcg(reinterpret_cast<int4*>(sc.dst[d] + base + idx * 16), packed);
+      }
+    }
+  }
+}
+
+template <typename T, int NSRC, int NLEV>
+__device__ __forceinline__ void fold_scalar(const SegCtx& sc, int64_t elem) {
+  using Tr = Traits<T>;
+  using B = typename Tr::Bits;
+  const int64_t byte = elem * (int64_t)sizeof(T);
+  if (NSRC == 1) {  // REPLACE: bitwise copy
+    const B v = __ldcg(reinterpret_cast<const B*>(sc.src[0] + byte));
+    for (int d = 0; d < sc.ndst; ++d) __stcg(reinterpret_cast<B*>(sc.dst[d] + byte), v);
+    return;
+  }
+  FoldState<T, 1, NLEV> st;
+#pragma unroll
+  for (int j = 0; j < NSRC; ++j) {
+    typename Tr::Acc x[1] = {Tr::from_bits(__ldcg(reinterpret_cast<const B*>(sc.src[j] + byte)))};
+    st.feed(sc.ctrl[j], x);
+  }
+  const B out = Tr::to_bits(st.result(0));
+  for (int d = 0; d < sc.ndst; ++d) __stcg(reinterpret_cast<B*>(sc.dst[d] + byte), out);
+}
+
+// (operand count, nesting depth) pairs that grid factorizations of <= 16 ranks produce.
+#ifndef RBX_FOLD_SHAPES
+#define RBX_FOLD_SHAPES(X)                                                                              \
+  X(1, 1) X(2, 1) X(3, 1) X(4, 1) X(5, 1) X(6, 1) X(7, 1) X(8, 1) X(9, 1) X(10, 1) X(11, 1) X(12, 1)     \
+  X(13, 1) X(14, 1) X(15, 1) X(16, 1) X(4, 2) X(6, 2) X(8, 2) X(9, 2) X(10, 2) X(12, 2) X(14, 2)         \
+  X(15, 2) X(16, 2) X(8, 3) X(12, 3) X(16, 3) X(16, 4)
+#endif
+
+template <typename T>
+__device__ __forceinline__ void dispatch_body(int nsrc, int nlev, const SegCtx& sc, int64_t body_off, int64_t v0,
+                                              int64_t v1) {
+  switch (nsrc * 8 + nlev) {
+#define RBX_CASE(N, L) \
+  case N * 8 + L:      \
+    fold_body<T, N, L>(sc, body_off, v0, v1); break;
+    RBX_FOLD_SHAPES(RBX_CASE)
+#undef RBX_CASE
+    default: break;
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void dispatch_scalar(int nsrc, int nlev, const SegCtx& sc, int64_t elem) {
+  switch (nsrc * 8 + nlev) {
+#define RBX_CASE(N, L) \
+  case N * 8 + L:      \
+    fold_scalar<T, N, L>(sc, elem); break;
+    RBX_FOLD_SHAPES(RBX_CASE)
+#undef RBX_CASE
+    default: break;
+  }
+}
+
+struct ErrRecord {  // host-mapped; first failure wins
+  int code, rank, step, peer;
+};
+
+struct KernelArgs {
+  const Plan* plans;     // one per rank hosted by this launch
+  int nblocks;           // CTAs per rank
+  uint64_t timeout_ns;
+  ErrRecord* err;
+};
+
+__device__ __forceinline__ bool flag_reached(uint32_t v, uint32_t e) { return (int32_t)(v - e) >= 0; }
+
+// Spin until flags[slot][peer][blk] >= e.  Returns false on timeout/abort.
+__device__ __forceinline__ bool spin_flag(const uint32_t* f, uint32_t e, volatile uint32_t* abort_word,
+                                          uint64_t t0, uint64_t timeout_ns) {
+  uint32_t it = 0;
+  while (!flag_reached(ld_acquire_sys(f), e)) {
+    if ((++it & 255u) == 0) {
+      if (*abort_word) return false;
+      if (global_ns() - t0 > timeout_ns) return false;
+      __nanosleep(64);
+    }
+  }
+  return true;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512, 1) rbx_step_kernel(KernelArgs args) {
+  const int vrank = blockIdx.x / args.nblocks;
+  const int b = blockIdx.x % args.nblocks;
+  const Plan& P = args.plans[vrank];
+  const int nb = args.nblocks;
+  __shared__ uint32_t s_epoch;
+  __shared__ int s_fail;
+  __shared__ SegCtx s_seg;
+  uint32_t* my_sig = P.my_sig;
+  volatile uint32_t* abort_word = my_sig ? (volatile uint32_t*)(my_sig + SigLayout::abort_off) : nullptr;
+  const uint64_t t0 = P.nosync ? 0 : global_ns();
+
+  if (threadIdx.x == 0) {
+    s_fail = 0;
+    s_epoch = P.nosync ? 0u : my_sig[SigLayout::epoch_off + b] + 1u;
+  }
+  __syncthreads();
+  const uint32_t e = s_epoch;
+
+  if (!P.nosync && threadIdx.x < P.nentry) {  // ENTRY: "my stream reached the collective"
+    __threadfence_system();
+    const int q = P.entry_peers[threadIdx.x];
+    st_release_sys(P.sig[q] + flag_index(0, P.me, b), e);
+  }
+
+  for (int s = 0; s < P.nsteps; ++s) {
+    const Step& st = P.steps[s];
+    // ---- wait ----
+    if (!P.nosync && st.nwait) {
+      bool ok = true;
+      for (int w = 0; w < st.nwait && ok; ++w) {
+        const Wait wt = P.waits[st.wait0 + w];
+        const uint32_t* base = my_sig + flag_index(wt.slot, wt.peer, 0);
+        if (wt.all) {
+          for (int k = threadIdx.x; k < nb && ok; k += blockDim.x) ok = spin_flag(base + k, e, abort_word, t0, args.timeout_ns);
+        } else if ((int)threadIdx.x == (w % blockDim.x)) {
+          ok = spin_flag(base + b, e, abort_word, t0, args.timeout_ns);
+        }
+        if (!ok) {
+          s_fail = 1;
+          if (atomicCAS(&args.err->code, 0, 3) == 0) {
+            args.err->rank = P.me;
+            args.err->step = s;
+            args.err->peer = wt.peer;
+          }
+          *abort_word = 1u;
+        }
+      }
+      __syncthreads();
+      if (s_fail) return;
+    }
+    // ---- work ----
+    const int64_t T_vec = st.total_vec;
+    const int64_t my0 = T_vec * b / nb, my1 = T_vec * (b + 1) / nb;
+    for (int k = 0; k < st.nseg; ++k) {
+      const Seg& sg = P.segs[st.seg0 + k];
+      const bool scalar_part = (sg.head + sg.tail) > 0 && (k % nb) == b;
+      const int64_t lo = my0 > sg.vec_begin ? my0 : sg.vec_begin;
+      const int64_t hi = my1 < sg.vec_begin + sg.nvec ? my1 : sg.vec_begin + sg.nvec;
+      if (!(lo < hi) && !scalar_part) continue;
+      __syncthreads();  // s_seg reuse
+      if (threadIdx.x < sg.nsrc) {
+        s_seg.src[threadIdx.x] = (const char*)P.ptrs[sg.tbl + sg.src[threadIdx.x]];
+        s_seg.ctrl[threadIdx.x] = sg.ctrl[threadIdx.x];
+      }
+      if (threadIdx.x < sg.ndst) s_seg.dst[threadIdx.x] = (char*)P.ptrs[sg.tbl + sg.dst[threadIdx.x]];
+      if (threadIdx.x == 0) {
+        s_seg.ndst = sg.ndst;
+        s_seg.nlev = sg.nlev;
+      }
+      __syncthreads();
+      if (lo < hi) dispatch_body<T>(sg.nsrc, sg.nlev, s_seg, sg.body_off, lo - sg.vec_begin, hi - sg.vec_begin);
+      if (scalar_part && (int)threadIdx.x < sg.head + sg.tail) {
+        const int64_t elem = threadIdx.x < sg.head ? sg.off + threadIdx.x
+                                                   : sg.body_off + sg.nvec * P.vec + (threadIdx.x - sg.head);
+        dispatch_scalar<T>(sg.nsrc, sg.nlev, s_seg, elem);
+      }
+    }
+    // ---- signal ----
+    if (!P.nosync && st.nsig) {
+      __syncthreads();
+      if ((int)threadIdx.x < st.nsig) {
+        __threadfence_system();
+        const int q = P.sigs[st.sig0 + threadIdx.x];
+        st_release_sys(P.sig[q] + flag_index(s + 1, P.me, b), e);
+      }
+    }
+  }
+  if (!P.nosync && threadIdx.x == 0) my_sig[SigLayout::epoch_off + b] = e;
+}
+
+}  // namespace rbx

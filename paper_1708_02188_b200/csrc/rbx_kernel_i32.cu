@@ -1,0 +1,6 @@
+// Instantiation of the step kernel for dtype i32 (one TU per dtype: parallel builds).
+#include "rbx_kernel.cuh"
+
+namespace rbx {
+const void* step_kernel_i32() { return reinterpret_cast<const void*>(&rbx_step_kernel<unsigned int>); }
+}  // namespace rbx

@@ -1,0 +1,73 @@
+"""All ranks of a grid on ONE GPU, in ONE launch.
+
+Two uses:
+* `mode="local"` -- the 1-GPU local-reduce roofline (north_star "1 GPU (local
+  reduce/copy roofline)"): every owned region is folded from the V rank
+  buffers in the reference order and written to all V buffers; HBM-bound,
+  no flags.
+* any other mode -- the exact multi-rank kernel (flags, epochs, pushes,
+  per-dimension stages) with each rank played by a CTA group of a single
+  cooperative launch, so the synchronisation logic is testable on one GPU
+  without running rank kernels that wait on each other as separate launches.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+from . import _native
+from .runtime import _dtype_name
+
+
+class VirtualRanks:
+    def __init__(self, dims, device: int = 0, nblocks_per_rank: int = 0, threads: int = 512, timeout_s: float = 30.0):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("VirtualRanks needs a CUDA device (no CPU fallback)")
+        self.dims = tuple(dims)
+        n = 1
+        for d in self.dims:
+            n *= d
+        self.nranks = n
+        self.device = torch.device("cuda", device)
+        self._L = _native.lib()
+        self._comm = ctypes.c_void_p()
+        _native.check(self._L.rbx_vcomm_create(ctypes.byref(self._comm), n, _native.ints(self.dims), len(self.dims),
+                                               device, nblocks_per_rank, threads))
+        self._L.rbx_comm_set_timeout(self._comm, float(timeout_s))
+
+    @property
+    def launches(self) -> int:
+        v = ctypes.c_uint64()
+        _native.check(self._L.rbx_comm_info(self._comm, None, None, None, None, ctypes.byref(v)))
+        return v.value
+
+    @property
+    def nblocks(self) -> int:
+        v = ctypes.c_int()
+        _native.check(self._L.rbx_comm_info(self._comm, None, None, ctypes.byref(v), None, None))
+        return v.value
+
+    def collective(self, tensors: list, op: str = "allreduce", mode: str = "fused", stream=None) -> None:
+        import torch
+
+        if len(tensors) != self.nranks:
+            raise ValueError(f"need {self.nranks} buffers, got {len(tensors)}")
+        n = tensors[0].numel()
+        dt = _dtype_name(tensors[0])
+        for t in tensors:
+            if t.numel() != n or _dtype_name(t) != dt or not t.is_contiguous() or t.device != self.device:
+                raise ValueError("virtual-rank buffers must match in length/dtype/device and be contiguous")
+        ptrs = (ctypes.c_void_p * self.nranks)(*[t.data_ptr() for t in tensors])
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _native.check(self._L.rbx_vcollective(self._comm, ptrs, n, _native.DTYPE_CODES[dt], _native.OPS[op],
+                                              _native.MODES[mode], ctypes.c_void_p(s.cuda_stream)))
+
+    def check(self) -> None:
+        _native.check(self._L.rbx_check(self._comm))
+
+    def close(self) -> None:
+        if self._comm:
+            self._L.rbx_comm_destroy(self._comm)
+            self._comm = None
