@@ -238,6 +238,9 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
   if (mode == RBX_MODE_LOCAL) return fail(RBX_ERR_INVALID, "MODE_LOCAL needs a virtual communicator");
   if (int rc = check_mode_dtype(mode, dtype)) return rc;
   if (c->err_host->code) return fail(RBX_ERR_COLLECTIVE, "communicator is in an error state", c->err_host->peer, c->err_host->step);
+  size_t total = 0;
+  for (int k = 0; k < nbufs; ++k) total += counts[k];
+  if (total == 0 && op != RBX_OP_BARRIER) return RBX_OK;  // empty collective: nothing moves on any rank
   std::vector<const void*> kp(bufs, bufs + nbufs);
   std::vector<size_t> kc(counts, counts + nbufs);
   const std::string key = plan_key(op, mode, dtype, kp, kc);

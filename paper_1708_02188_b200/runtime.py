@@ -285,6 +285,9 @@ class RankContext:
         dt = _dtype_name(tensor)
         n = tensor.numel()
         m = _native.MODES[mode or self.mode]
+        if n == 0:
+            self._agree_shape((tensor.data_ptr(), op, n, dt, m))
+            return (0, 0)
         self._ensure(tensor)
         self._agree_shape((tensor.data_ptr(), op, n, dt, m))
         code = _native.DTYPE_CODES[dt]
