@@ -215,6 +215,21 @@ int check_mode_dtype(int mode, int dtype) {
   return RBX_OK;
 }
 
+// Elements between the previous 16-byte boundary and element 0, if identical
+// for every rank's copy (then the scalar head/tail peel is the same
+// everywhere); -1 if the copies are differently aligned (scalar path only).
+int misalign(const std::vector<void*>& ptrs, int es) {
+  int m = -1;
+  for (void* p : ptrs) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    if (a % es) return -1;
+    const int mm = (int)((a % 16) / es);
+    if (m >= 0 && mm != m) return -1;
+    m = mm;
+  }
+  return m < 0 ? 0 : m;
+}
+
 int find_buffer(rbx_comm* c, const void* p, size_t bytes, int* id, size_t* off) {
   for (size_t i = 0; i < c->bufs.size(); ++i) {
     const RegBuf& b = c->bufs[i];
@@ -257,10 +272,15 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
     for (int k = 0; k < nbufs; ++k) {
       int id;
       size_t off;
-      if (op != RBX_OP_BARRIER) {
+      if (op != RBX_OP_BARRIER && counts[k] == 0) {
+        for (int q = 0; q < c->nranks; ++q) ptrs.push_back(nullptr);  // empty bucket: never dereferenced
+      } else if (op != RBX_OP_BARRIER) {
         int rc = find_buffer(c, bufs[k], counts[k] * es, &id, &off);
         if (rc) return rc;
-        for (int q = 0; q < c->nranks; ++q) ptrs.push_back(c->bufs[id].at[q] + off);
+        std::vector<void*> mine;
+        for (int q = 0; q < c->nranks; ++q) mine.push_back(c->bufs[id].at[q] + off);
+        spec.mis = misalign(mine, es);
+        ptrs.insert(ptrs.end(), mine.begin(), mine.end());
       }
       if (!rbx::build_plan(c->geo, c->rank, (int64_t)counts[k], spec, k * c->nranks, &host[0], k == 0, &err))
         return fail(RBX_ERR_INVALID, err);
@@ -324,7 +344,7 @@ int64_t rbx_plan_describe(const int* dims, int ndims, int rank, int64_t count, i
   std::unique_ptr<rbx::Plan> p(new rbx::Plan);
   bool ok;
   if (mode == RBX_MODE_LOCAL)
-    ok = rbx::build_local_plan(g, count, 16 / es, 148, p.get(), &err);
+    ok = rbx::build_local_plan(g, count, 16 / es, 0, 148, p.get(), &err);
   else {
     if (rank < 0 || rank >= g.nranks) return fail(RBX_ERR_INVALID, "rank out of range"), -1;
     rbx::PlanSpec spec;
@@ -578,13 +598,16 @@ int rbx_vcollective(rbx_comm_t* c, void* const* bufs, size_t count, int dtype, i
     std::string err;
     std::vector<void*> ptrs(bufs, bufs + V);
     std::vector<rbx::Plan> host(local ? 1 : V);
+    const int mis = misalign(ptrs, es);
     if (local) {
-      if (!rbx::build_local_plan(c->geo, (int64_t)count, 16 / es, nb, &host[0], &err)) return fail(RBX_ERR_INVALID, err);
+      if (!rbx::build_local_plan(c->geo, (int64_t)count, 16 / es, mis, nb, &host[0], &err))
+        return fail(RBX_ERR_INVALID, err);
     } else {
       rbx::PlanSpec spec;
       spec.op = (rbx::Op)op;
       spec.mode = (rbx::Mode)mode;
       spec.vec = 16 / es;
+      spec.mis = mis;
       spec.nblocks = nb;
       for (int r = 0; r < V; ++r) {
         if (!rbx::build_plan(c->geo, r, (int64_t)count, spec, 0, &host[r], true, &err)) return fail(RBX_ERR_INVALID, err);

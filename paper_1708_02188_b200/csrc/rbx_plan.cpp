@@ -218,7 +218,7 @@ std::vector<uint8_t> single_level_ctrl(size_t n) {
 
 }  // namespace
 
-static bool add_segments(Plan* p, std::vector<SegProto>& segs, int tbl, int vec, std::string* err) {
+static bool add_segments(Plan* p, std::vector<SegProto>& segs, int tbl, int vec, int mis, std::string* err) {
   // Segments are stored grouped by step; merge into the existing layout.
   std::vector<Seg> all;
   std::vector<int> owner;
@@ -232,9 +232,14 @@ static bool add_segments(Plan* p, std::vector<SegProto>& segs, int tbl, int vec,
     std::memset(&sg, 0, sizeof(sg));
     sg.off = sp.off;
     sg.len = sp.len;
-    const int64_t mis = sp.off % vec;
-    int64_t head = mis ? (vec - mis) : 0;
-    if (head > sp.len) head = sp.len;
+    // scalar head up to the first 16-byte aligned element (the base of the
+    // buffer is `mis` elements past a 16-byte boundary on every rank)
+    int64_t head = sp.len;
+    if (mis >= 0) {
+      const int64_t phase = (mis + sp.off) % vec;
+      head = phase ? (vec - phase) : 0;
+      if (head > sp.len) head = sp.len;
+    }
     sg.head = (int32_t)head;
     sg.body_off = sp.off + head;
     sg.nvec = (sp.len - head) / vec;
@@ -435,10 +440,10 @@ bool build_plan(const Geometry& g, int me, int64_t count, const PlanSpec& spec, 
     if (err) *err = "bucket plans disagree in structure";
     return false;
   }
-  return add_segments(p, segs, tbl, spec.vec, err);
+  return add_segments(p, segs, tbl, spec.vec, spec.mis, err);
 }
 
-bool build_local_plan(const Geometry& g, int64_t count, int vec, int nblocks, Plan* p, std::string* err) {
+bool build_local_plan(const Geometry& g, int64_t count, int vec, int mis, int nblocks, Plan* p, std::string* err) {
   std::memset(p, 0, sizeof(Plan));
   p->me = 0;
   p->nranks = g.nranks;
@@ -458,7 +463,7 @@ bool build_local_plan(const Geometry& g, int64_t count, int vec, int nblocks, Pl
     region_after(g, r, count, m, &o, &l);
     segs.push_back(SegProto{0, o, l, fold_order(g, r), ctrl, m, rotated_after(everyone, r)});
   }
-  return add_segments(p, segs, 0, vec, err);
+  return add_segments(p, segs, 0, vec, mis, err);
 }
 
 int64_t describe_plan(const Plan& p, int64_t* out, int64_t cap) {

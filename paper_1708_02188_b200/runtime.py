@@ -249,6 +249,8 @@ class RankContext:
         self._registered[ptr] = (nbytes, tensor)
 
     def _ensure(self, tensor) -> None:
+        if tensor.numel() == 0:
+            return
         ptr = tensor.data_ptr()
         for base, (nb, _) in self._registered.items():
             if base <= ptr and ptr + tensor.numel() * tensor.element_size() <= base + nb:
@@ -499,7 +501,15 @@ def launch(ranks: int, plan, workload: Workload, rendezvous=None, timeout_s: flo
             pending.discard(r)
         else:
             _, r, culprit, phase, text = msg
-            dead = [x for x, p in procs.items() if x in pending and not p.is_alive() and p.exitcode not in (0, None)]
+            # A peer that died makes the survivors fail too (lost connection or
+            # watchdog); give the dead process a moment to be reaped so the
+            # failure is attributed to it, as the reference's liveness polling does.
+            dead = []
+            t_wait = time.monotonic() + 5.0
+            while not dead and time.monotonic() < t_wait:
+                dead = [x for x, p in procs.items() if not p.is_alive() and p.exitcode not in (0, None)]
+                if not dead:
+                    time.sleep(0.1)
             if dead:
                 culprit = dead[0]
             suffix = f" (phase {phase})" if phase is not None else ""
