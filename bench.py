@@ -54,6 +54,7 @@ def parse_args():
     p.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-nccl", action="store_true")
+    p.add_argument("--e2e-chunks", type=int, default=8, help="pipeline windows for the host-buffer e2e leg")
     return p.parse_args()
 
 
@@ -126,6 +127,43 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
                 "samples": len(sm)}
+
+
+def pipelined_e2e(n, chunks, h2d, red, d2h, stream, iters, warmup, before):
+    """Time host->device->host steps: window k's H2D, reduction and D2H run on
+    three streams so PCIe in both directions overlaps the kernels.  Returns
+    per-step milliseconds (CUDA events on `stream`, which brackets the step)."""
+    import torch
+
+    s_in, s_red, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    bounds = [(n * k // chunks, n * (k + 1) // chunks) for k in range(chunks)]
+    out = []
+    for it in range(iters):
+        before()
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for st in (s_in, s_red, s_out):
+            st.wait_event(start)
+        for lo, hi in bounds:
+            with torch.cuda.stream(s_in):
+                h2d(lo, hi)
+            ev_in = torch.cuda.Event()
+            ev_in.record(s_in)
+            s_red.wait_event(ev_in)
+            red(lo, hi, s_red)
+            ev_red = torch.cuda.Event()
+            ev_red.record(s_red)
+            s_out.wait_event(ev_red)
+            with torch.cuda.stream(s_out):
+                d2h(lo, hi)
+        ev_done = torch.cuda.Event()
+        ev_done.record(s_out)
+        stream.wait_event(ev_done)
+        end.record(stream)
+        torch.cuda.synchronize()
+        if it >= warmup:
+            out.append(start.elapsed_time(end))
+    return out
 
 
 def busbw(ranks: int, nbytes: int, seconds: float) -> float:
@@ -246,24 +284,29 @@ def main_single(args):
     bw = busbw(ranks, nbytes, t)
 
     # e2e through the C ABI with HOST buffers: pinned H2D of every rank's input,
-    # the collective, D2H of every rank's result -- all inside the timed region.
+    # the collective, D2H of every rank's result -- all inside the timed region,
+    # pipelined over element windows on three streams (copy-in / reduce / copy-out).
     pinned = [h.pin_memory() for h in host]
     outs = [torch.empty_like(h).pin_memory() for h in host]
-    e2e_ms = []
-    for k in range(args.warmup + max(3, min(args.steps, 10))):
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        scratch.fill_(1.0)
-        s.record(stream)
+
+    def h2d(lo, hi):
         for w, h in zip(work, pinned):
-            w.copy_(h, non_blocking=True)
-        vr.collective(work, mode="local")
+            w[lo:hi].copy_(h[lo:hi], non_blocking=True)
+
+    def d2h(lo, hi):
         for o, w in zip(outs, work):
-            o.copy_(w, non_blocking=True)
-        e.record(stream)
-        torch.cuda.synchronize()
-        if k >= args.warmup:
-            e2e_ms.append(s.elapsed_time(e))
+            o[lo:hi].copy_(w[lo:hi], non_blocking=True)
+
+    def red(lo, hi, st):
+        vr.collective(work, mode="local", stream=st, window=(lo, hi))
+
+    e2e_ms = pipelined_e2e(n, args.e2e_chunks, h2d, red, d2h, stream, args.warmup + max(3, min(args.steps, 10)),
+                           args.warmup, lambda: scratch.fill_(1.0))
     t_e2e = statistics.mean(e2e_ms) / 1e3
+    restore()
+    vr.collective(work, mode="local")
+    torch.cuda.synchronize()
+    e2e_ok = all(torch.equal(o, w.cpu()) for o, w in zip(outs[:2], work[:2]))
 
     peak, peak_src = hbm_peak()
     hbm_bytes = 2 * ranks * nbytes  # read every rank buffer once, write every rank buffer once
@@ -296,7 +339,7 @@ def main_single(args):
         "cpu_baseline": cpu,
         "e2e": {"value": round(busbw(ranks, nbytes, t_e2e), 4), "unit": "GB/s",
                 "h2d_bytes_per_step": ranks * nbytes, "d2h_bytes_per_step": ranks * nbytes,
-                "ms_per_step": round(t_e2e * 1e3, 3)},
+                "ms_per_step": round(t_e2e * 1e3, 3), "chunks": args.e2e_chunks, "result_matches_device_path": e2e_ok},
         "gpu_launches": launches,
         "clocks": clocks,
         "step_ms": [round(x, 4) for x in step_ms],
@@ -367,25 +410,27 @@ def main_multi(args):
     nbytes = n * esz
     bw = busbw(world, nbytes, t)
 
-    # e2e: pinned host buffer -> H2D -> allreduce -> D2H inside the timed region
+    # e2e: pinned host buffer -> H2D -> allreduce -> D2H inside the timed region,
+    # pipelined over element windows (rbx_allreduce_window) on three streams
     pinned = host.pin_memory()
     out = torch.empty_like(host).pin_memory()
-    e2e = []
-    for k in range(args.warmup + max(3, min(args.steps, 10))):
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        scratch.fill_(1.0)
-        ctx.barrier()
-        s.record(stream)
-        work.copy_(pinned, non_blocking=True)
-        ctx.collective("allreduce", work)
-        out.copy_(work, non_blocking=True)
-        e.record(stream)
-        torch.cuda.synchronize()
-        if k >= args.warmup:
-            e2e.append(s.elapsed_time(e))
+
+    def h2d(lo, hi):
+        work[lo:hi].copy_(pinned[lo:hi], non_blocking=True)
+
+    def d2h(lo, hi):
+        out[lo:hi].copy_(work[lo:hi], non_blocking=True)
+
+    def red(lo, hi, st):
+        with torch.cuda.stream(st):
+            ctx.allreduce_window(work, lo, hi)
+
+    e2e = pipelined_e2e(n, args.e2e_chunks, h2d, red, d2h, stream, args.warmup + max(3, min(args.steps, 10)),
+                        args.warmup, lambda: (scratch.fill_(1.0), ctx.barrier()))
     e2e_t = torch.tensor(e2e, device=dev)
     dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     t_e2e = e2e_t.mean().item() / 1e3
+    ctx.check()
 
     nccl = None
     if not args.no_nccl:
@@ -427,7 +472,8 @@ def main_multi(args):
             "nccl_busbw_gbs": nccl,
             "cpu_baseline": None,
             "e2e": {"value": round(busbw(world, nbytes, t_e2e) * world, 3), "unit": "GB/s",
-                    "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": round(t_e2e * 1e3, 3)},
+                    "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": round(t_e2e * 1e3, 3),
+                    "chunks": args.e2e_chunks},
             "gpu_launches": launches,
             "clocks": clocks,
         }

@@ -108,6 +108,11 @@ int rbx_allgather(rbx_comm_t *comm, void *buf, size_t count, int dtype, int mode
 /* One launch over a bucket list; Workload.lengths semantics (runtime.py:82-91, 390-398), buckets concurrent. */
 int rbx_allreduce_buckets(rbx_comm_t *comm, void *const *bufs, const size_t *counts, int nbufs, int dtype,
                           int mode, void *stream);
+/* Allreduce of the element window [lo, hi) of a count-element buffer with the FULL buffer's chunk
+ * geometry and reduction order (bit-identical to those elements of rbx_allreduce). Lets callers
+ * pipeline H2D / reduce / D2H or reduce a bucket as its gradients become ready. */
+int rbx_allreduce_window(rbx_comm_t *comm, void *buf, size_t count, size_t lo, size_t hi, int dtype, int mode,
+                         void *stream);
 /* Device-side flag barrier across all ranks (no data). */
 int rbx_barrier(rbx_comm_t *comm, void *stream);
 /* After the stream has been synchronised: RBX_ERR_COLLECTIVE if a watchdog fired. */
@@ -118,6 +123,8 @@ int rbx_vcomm_create(rbx_comm_t **comm, int nranks, const int *dims, int ndims, 
                      int threads);
 /* bufs[r] = rank r's device buffer.  mode RBX_MODE_LOCAL = the 1-GPU local reduce (no flags). */
 int rbx_vcollective(rbx_comm_t *comm, void *const *bufs, size_t count, int dtype, int op, int mode, void *stream);
+int rbx_vcollective_window(rbx_comm_t *comm, void *const *bufs, size_t count, size_t lo, size_t hi, int dtype, int op,
+                           int mode, void *stream);
 
 #ifdef __cplusplus
 }

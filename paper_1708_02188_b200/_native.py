@@ -77,6 +77,8 @@ def lib() -> ctypes.CDLL:
     _sig(L.rbx_reduce_scatter, c_int, _VP, _VP, c_size, c_int, c_int, _VP, _I64P, _I64P)
     _sig(L.rbx_allgather, c_int, _VP, _VP, c_size, c_int, c_int, _VP)
     _sig(L.rbx_allreduce_buckets, c_int, _VP, ctypes.POINTER(_VP), ctypes.POINTER(c_size), c_int, c_int, c_int, _VP)
+    _sig(L.rbx_allreduce_window, c_int, _VP, _VP, c_size, c_size, c_size, c_int, c_int, _VP)
+    _sig(L.rbx_vcollective_window, c_int, _VP, ctypes.POINTER(_VP), c_size, c_size, c_size, c_int, c_int, c_int, _VP)
     _sig(L.rbx_barrier, c_int, _VP, _VP)
     _sig(L.rbx_check, c_int, _VP)
     _sig(L.rbx_vcomm_create, c_int, ctypes.POINTER(_VP), c_int, _INTP, c_int, c_int, c_int, c_int)
@@ -91,8 +93,8 @@ EXPORTED = [
     "rbx_version", "rbx_last_error", "rbx_chunk_bounds", "rbx_owned_region", "rbx_fold_order", "rbx_plan_describe",
     "rbx_device_count", "rbx_alloc_symmetric", "rbx_free", "rbx_export_buffer", "rbx_comm_create",
     "rbx_comm_connect", "rbx_comm_destroy", "rbx_comm_set_timeout", "rbx_comm_info", "rbx_register_buffer",
-    "rbx_allreduce", "rbx_reduce_scatter", "rbx_allgather", "rbx_allreduce_buckets", "rbx_barrier", "rbx_check",
-    "rbx_vcomm_create", "rbx_vcollective",
+    "rbx_allreduce", "rbx_reduce_scatter", "rbx_allgather", "rbx_allreduce_buckets", "rbx_allreduce_window",
+    "rbx_barrier", "rbx_check", "rbx_vcomm_create", "rbx_vcollective", "rbx_vcollective_window",
 ]
 
 

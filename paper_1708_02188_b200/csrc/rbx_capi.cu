@@ -245,7 +245,7 @@ int find_buffer(rbx_comm* c, const void* p, size_t bytes, int* id, size_t* off) 
 }
 
 int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nbufs, int dtype, int op, int mode,
-                    cudaStream_t stream) {
+                    cudaStream_t stream, int64_t lo = 0, int64_t hi = -1) {
   if (!c || c->nvirtual) return fail(RBX_ERR_INVALID, "not a per-rank communicator");
   if (!c->connected) return fail(RBX_ERR_INVALID, "communicator is not connected");
   const int es = dtype_size(dtype);
@@ -258,7 +258,7 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
   if (total == 0 && op != RBX_OP_BARRIER) return RBX_OK;  // empty collective: nothing moves on any rank
   std::vector<const void*> kp(bufs, bufs + nbufs);
   std::vector<size_t> kc(counts, counts + nbufs);
-  const std::string key = plan_key(op, mode, dtype, kp, kc);
+  const std::string key = plan_key(op, mode, dtype, kp, kc) + "@" + std::to_string(lo) + ":" + std::to_string(hi);
   auto it = c->plans.find(key);
   if (it == c->plans.end()) {
     std::vector<rbx::Plan> host(1);
@@ -268,6 +268,8 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
     spec.mode = (rbx::Mode)mode;
     spec.vec = 16 / es;
     spec.nblocks = c->nblocks;
+    spec.lo = lo;
+    spec.hi = hi;
     std::string err;
     for (int k = 0; k < nbufs; ++k) {
       int id;
@@ -580,6 +582,21 @@ int rbx_vcomm_create(rbx_comm_t** comm, int nranks, const int* dims, int ndims, 
 }
 
 int rbx_vcollective(rbx_comm_t* c, void* const* bufs, size_t count, int dtype, int op, int mode, void* stream) {
+  return rbx_vcollective_window(c, bufs, count, 0, count, dtype, op, mode, stream);
+}
+
+int rbx_allreduce_window(rbx_comm_t* c, void* buf, size_t count, size_t lo, size_t hi, int dtype, int mode,
+                         void* stream) {
+  if (lo > hi || hi > count) return fail(RBX_ERR_INVALID, "window must satisfy lo <= hi <= count");
+  void* bufs[1] = {buf};
+  size_t counts[1] = {count};
+  return real_collective(c, bufs, counts, 1, dtype, RBX_OP_ALLREDUCE, mode, (cudaStream_t)stream, (int64_t)lo,
+                         (int64_t)hi);
+}
+
+int rbx_vcollective_window(rbx_comm_t* c, void* const* bufs, size_t count, size_t lo, size_t hi, int dtype, int op,
+                           int mode, void* stream) {
+  if (lo > hi || hi > count) return fail(RBX_ERR_INVALID, "window must satisfy lo <= hi <= count");
   if (!c || !c->nvirtual) return fail(RBX_ERR_INVALID, "not a virtual communicator");
   const int es = dtype_size(dtype);
   if (!es) return fail(RBX_ERR_INVALID, "unknown dtype");
@@ -587,7 +604,8 @@ int rbx_vcollective(rbx_comm_t* c, void* const* bufs, size_t count, int dtype, i
   if (int rc = check_mode_dtype(mode, dtype)) return rc;
   const int V = c->nvirtual;
   std::vector<const void*> kp(bufs, bufs + V);
-  const std::string key = plan_key(op, mode, dtype, kp, {count});
+  const std::string key =
+      plan_key(op, mode, dtype, kp, {count}) + "@" + std::to_string(lo) + ":" + std::to_string(hi);
   auto it = c->plans.find(key);
   const bool local = (mode == RBX_MODE_LOCAL);
   if (local && op != RBX_OP_ALLREDUCE) return fail(RBX_ERR_INVALID, "MODE_LOCAL supports allreduce only");
@@ -600,7 +618,7 @@ int rbx_vcollective(rbx_comm_t* c, void* const* bufs, size_t count, int dtype, i
     std::vector<rbx::Plan> host(local ? 1 : V);
     const int mis = misalign(ptrs, es);
     if (local) {
-      if (!rbx::build_local_plan(c->geo, (int64_t)count, 16 / es, mis, nb, &host[0], &err))
+      if (!rbx::build_local_plan(c->geo, (int64_t)count, 16 / es, mis, nb, &host[0], &err, (int64_t)lo, (int64_t)hi))
         return fail(RBX_ERR_INVALID, err);
     } else {
       rbx::PlanSpec spec;
@@ -609,6 +627,8 @@ int rbx_vcollective(rbx_comm_t* c, void* const* bufs, size_t count, int dtype, i
       spec.vec = 16 / es;
       spec.mis = mis;
       spec.nblocks = nb;
+      spec.lo = (int64_t)lo;
+      spec.hi = (int64_t)hi;
       for (int r = 0; r < V; ++r) {
         if (!rbx::build_plan(c->geo, r, (int64_t)count, spec, 0, &host[r], true, &err)) return fail(RBX_ERR_INVALID, err);
         for (int q = 0; q < V; ++q) host[r].sig[q] = c->sig[q];

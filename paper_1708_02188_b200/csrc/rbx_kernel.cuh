@@ -411,10 +411,11 @@ __global__ void __launch_bounds__(512, 1) rbx_step_kernel(KernelArgs args) {
       }
       __syncthreads();
       if (lo < hi) dispatch_body<T>(sg.nsrc, sg.nlev, s_seg, sg.body_off, lo - sg.vec_begin, hi - sg.vec_begin);
-      if (scalar_part && (int)threadIdx.x < sg.head + sg.tail) {
-        const int64_t elem = threadIdx.x < sg.head ? sg.off + threadIdx.x
-                                                   : sg.body_off + sg.nvec * P.vec + (threadIdx.x - sg.head);
-        dispatch_scalar<T>(sg.nsrc, sg.nlev, s_seg, elem);
+      if (scalar_part) {
+        for (int i = threadIdx.x; i < sg.head + sg.tail; i += blockDim.x) {
+          const int64_t elem = i < sg.head ? sg.off + i : sg.body_off + sg.nvec * P.vec + (i - sg.head);
+          dispatch_scalar<T>(sg.nsrc, sg.nlev, s_seg, elem);
+        }
       }
     }
     // ---- signal ----

@@ -218,7 +218,8 @@ std::vector<uint8_t> single_level_ctrl(size_t n) {
 
 }  // namespace
 
-static bool add_segments(Plan* p, std::vector<SegProto>& segs, int tbl, int vec, int mis, std::string* err) {
+static bool add_segments(Plan* p, std::vector<SegProto>& segs, int tbl, int vec, int mis, int64_t lo, int64_t hi,
+                         std::string* err) {
   // Segments are stored grouped by step; merge into the existing layout.
   std::vector<Seg> all;
   std::vector<int> owner;
@@ -230,20 +231,28 @@ static bool add_segments(Plan* p, std::vector<SegProto>& segs, int tbl, int vec,
   for (const SegProto& sp : segs) {
     Seg sg;
     std::memset(&sg, 0, sizeof(sg));
-    sg.off = sp.off;
-    sg.len = sp.len;
+    // restrict to the element window [lo, hi): every operation is
+    // element-wise, so a window keeps the full-buffer chunk geometry and order
+    int64_t a = sp.off > lo ? sp.off : lo, b = sp.off + sp.len < hi ? sp.off + sp.len : hi;
+    if (b < a) b = a;
+    sg.off = a;
+    sg.len = b - a;
     // scalar head up to the first 16-byte aligned element (the base of the
     // buffer is `mis` elements past a 16-byte boundary on every rank)
-    int64_t head = sp.len;
+    int64_t head = sg.len;
     if (mis >= 0) {
-      const int64_t phase = (mis + sp.off) % vec;
+      const int64_t phase = (mis + sg.off) % vec;
       head = phase ? (vec - phase) : 0;
-      if (head > sp.len) head = sp.len;
+      if (head > sg.len) head = sg.len;
     }
-    sg.head = (int32_t)head;
-    sg.body_off = sp.off + head;
-    sg.nvec = (sp.len - head) / vec;
-    sg.tail = (int32_t)(sp.len - head - sg.nvec * vec);
+    sg.head = (int32_t)(head < (1 << 30) ? head : (1 << 30));
+    if (head >= (1 << 30)) {
+      if (err) *err = "misaligned segment too long for the scalar path";
+      return false;
+    }
+    sg.body_off = sg.off + head;
+    sg.nvec = (sg.len - head) / vec;
+    sg.tail = (int32_t)(sg.len - head - sg.nvec * vec);
     sg.tbl = tbl;
     sg.nsrc = (uint8_t)sp.src.size();
     sg.ndst = (uint8_t)sp.dst.size();
@@ -440,10 +449,11 @@ bool build_plan(const Geometry& g, int me, int64_t count, const PlanSpec& spec, 
     if (err) *err = "bucket plans disagree in structure";
     return false;
   }
-  return add_segments(p, segs, tbl, spec.vec, spec.mis, err);
+  return add_segments(p, segs, tbl, spec.vec, spec.mis, spec.lo, spec.hi < 0 ? count : spec.hi, err);
 }
 
-bool build_local_plan(const Geometry& g, int64_t count, int vec, int mis, int nblocks, Plan* p, std::string* err) {
+bool build_local_plan(const Geometry& g, int64_t count, int vec, int mis, int nblocks, Plan* p, std::string* err,
+                      int64_t lo, int64_t hi) {
   std::memset(p, 0, sizeof(Plan));
   p->me = 0;
   p->nranks = g.nranks;
@@ -463,7 +473,7 @@ bool build_local_plan(const Geometry& g, int64_t count, int vec, int mis, int nb
     region_after(g, r, count, m, &o, &l);
     segs.push_back(SegProto{0, o, l, fold_order(g, r), ctrl, m, rotated_after(everyone, r)});
   }
-  return add_segments(p, segs, 0, vec, mis, err);
+  return add_segments(p, segs, 0, vec, mis, lo, hi < 0 ? count : hi, err);
 }
 
 int64_t describe_plan(const Plan& p, int64_t* out, int64_t cap) {

@@ -120,6 +120,7 @@ struct PlanSpec {
   Mode mode = MODE_FUSED;
   int vec = 4;             // elements per 16B vector of the dtype
   int mis = 0;             // (base address % 16) / itemsize, same on every rank; -1: never vectorise
+  int64_t lo = 0, hi = -1; // element window [lo, hi) (hi < 0: whole buffer)
   int nblocks = 148;
 };
 
@@ -129,7 +130,8 @@ struct PlanSpec {
 bool build_plan(const Geometry& g, int rank, int64_t count, const PlanSpec& spec, int tbl, Plan* p,
                 bool first, std::string* err);
 // Local (single-GPU, no synchronisation) plan over all virtual ranks' buffers.
-bool build_local_plan(const Geometry& g, int64_t count, int vec, int mis, int nblocks, Plan* p, std::string* err);
+bool build_local_plan(const Geometry& g, int64_t count, int vec, int mis, int nblocks, Plan* p, std::string* err,
+                      int64_t lo = 0, int64_t hi = -1);
 // Flatten a plan into int64s for host-side inspection (tests).
 int64_t describe_plan(const Plan& p, int64_t* out, int64_t cap);
 

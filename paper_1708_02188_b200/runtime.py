@@ -311,6 +311,21 @@ class RankContext:
             self.synchronize()
         return owned
 
+    def allreduce_window(self, tensor, lo: int, hi: int, mode: str | None = None) -> None:
+        """Allreduce only elements [lo, hi) of `tensor`, with the full buffer's
+        chunk geometry and order (bit-identical to those elements of a full call)."""
+        dt = _dtype_name(tensor)
+        n = tensor.numel()
+        m = _native.MODES[mode or self.mode]
+        if not 0 <= lo <= hi <= n:
+            raise ValueError(f"window [{lo}, {hi}) outside [0, {n}]")
+        self._ensure(tensor)
+        self._agree_shape((tensor.data_ptr(), "window", n, lo, hi, dt, m))
+        _native.check(self._L.rbx_allreduce_window(self._comm, ctypes.c_void_p(tensor.data_ptr()), n, lo, hi,
+                                                   _native.DTYPE_CODES[dt], m, self.stream()))
+        if self.blocking:
+            self.synchronize()
+
     def allreduce_buckets(self, tensors, mode: str | None = None) -> None:
         """All buckets of a list in ONE launch (concurrent rings); each bucket is
         chunked independently exactly like Workload.lengths entries (runtime.py:390-398)."""

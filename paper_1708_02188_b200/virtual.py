@@ -49,7 +49,9 @@ class VirtualRanks:
         _native.check(self._L.rbx_comm_info(self._comm, None, None, ctypes.byref(v), None, None))
         return v.value
 
-    def collective(self, tensors: list, op: str = "allreduce", mode: str = "fused", stream=None) -> None:
+    def collective(self, tensors: list, op: str = "allreduce", mode: str = "fused", stream=None, window=None) -> None:
+        """window=(lo, hi): only elements [lo, hi), with the full buffers' chunk
+        geometry and reduction order (bit-identical to a full call there)."""
         import torch
 
         if len(tensors) != self.nranks:
@@ -61,8 +63,10 @@ class VirtualRanks:
                 raise ValueError("virtual-rank buffers must match in length/dtype/device and be contiguous")
         ptrs = (ctypes.c_void_p * self.nranks)(*[t.data_ptr() for t in tensors])
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        _native.check(self._L.rbx_vcollective(self._comm, ptrs, n, _native.DTYPE_CODES[dt], _native.OPS[op],
-                                              _native.MODES[mode], ctypes.c_void_p(s.cuda_stream)))
+        lo, hi = window if window is not None else (0, n)
+        _native.check(self._L.rbx_vcollective_window(self._comm, ptrs, n, lo, hi, _native.DTYPE_CODES[dt],
+                                                     _native.OPS[op], _native.MODES[mode],
+                                                     ctypes.c_void_p(s.cuda_stream)))
 
     def check(self) -> None:
         _native.check(self._L.rbx_check(self._comm))

@@ -178,3 +178,28 @@ def test_repeated_calls_epochs_and_launch_count():
             assert np.array_equal(t.cpu().numpy(), want)
     assert vr.launches - base == 12
     vr.close()
+
+
+@pytest.mark.parametrize("mode", ["local", "fused", "ring_dims"])
+def test_windows_compose_to_the_full_allreduce(mode):
+    """rbx_vcollective_window: element windows keep the full buffer's chunk
+    geometry and order, so any split reproduces the full result bit-for-bit."""
+    torch = _torch()
+    from paper_1708_02188_b200.virtual import VirtualRanks
+
+    for dims in [(2, 2, 2), (2, 4), (3, 2)]:
+        n = int(np.prod(dims))
+        grid = orc.Grid(dims)
+        length = 100_003
+        parts = [orc.generate_input(9, 0, r, length, "f32") for r in range(n)]
+        want = orc.closed_form_allreduce(grid, parts)
+        vr = VirtualRanks(dims, nblocks_per_rank=0 if mode == "local" else 4)
+        ts = [torch.from_numpy(p.copy()).cuda() for p in parts]
+        cuts = [0, 1, 7777, 50_000, 50_001, 99_999, length]
+        for lo, hi in zip(cuts[:-1], cuts[1:]):
+            vr.collective(ts, mode=mode, window=(lo, hi))
+        torch.cuda.synchronize()
+        vr.check()
+        for t in ts:
+            assert np.array_equal(t.cpu().numpy(), want)
+        vr.close()
