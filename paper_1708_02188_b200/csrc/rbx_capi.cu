@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -70,6 +71,7 @@ struct CachedPlan {
   rbx::Plan* dev = nullptr;  // nplans contiguous plans
   void** ptrs = nullptr;
   int nplans = 0;
+  int plan_bytes = 0;  // staged into shared memory by every CTA
 };
 
 struct OpenedHandle {
@@ -95,6 +97,7 @@ struct rbx_comm {
   bool connected = false;
   int sm_count = 148;
   int max_coresident = 0;  // co-resident CTAs of the step kernel
+  int tile = 0;            // work tile in 16-byte vectors (0: contiguous range per CTA); env RBX_TILE
 };
 
 namespace {
@@ -138,9 +141,11 @@ int coresident_blocks(int device, int threads, int* out) {
   int sms = 0;
   RBX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   int worst = 1 << 30;
+  const size_t max_smem = (rbx::plan_smem_bytes(RBX_MAX_SEGS) + 15) / 16 * 16;
   for (int dt = RBX_F32; dt <= RBX_I32; ++dt) {
+    RBX_CUDA(cudaFuncSetAttribute(kernel_for(dt), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem));
     int per_sm = 0;
-    RBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_for(dt), threads, 0));
+    RBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_for(dt), threads, max_smem));
     if (per_sm * sms < worst) worst = per_sm * sms;
   }
   *out = worst;
@@ -154,6 +159,7 @@ int common_init(rbx_comm* c, const int* dims, int ndims, int device, int threads
   if (threads % 32 || threads > 512) return fail(RBX_ERR_INVALID, "threads must be a multiple of 32 and <= 512");
   c->threads = threads;
   c->device = device;
+  if (const char* t = std::getenv("RBX_TILE")) c->tile = std::atoi(t);
   RBX_CUDA(cudaSetDevice(device));
   RBX_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
   int rc = coresident_blocks(device, threads, &c->max_coresident);
@@ -178,7 +184,15 @@ int upload(rbx_comm* c, std::vector<rbx::Plan>& host, const std::vector<void*>& 
   RBX_CUDA(cudaMalloc(reinterpret_cast<void**>(&out->ptrs), sizeof(void*) * (ptrs.size() ? ptrs.size() : 1)));
   if (!ptrs.empty())
     RBX_CUDA(cudaMemcpy(out->ptrs, ptrs.data(), sizeof(void*) * ptrs.size(), cudaMemcpyHostToDevice));
-  for (auto& p : host) p.ptrs = out->ptrs;
+  int maxsegs = 0;
+  for (auto& p : host) {
+    p.ptrs = out->ptrs;
+    p.tile = c->tile;
+    int segs = 0;
+    for (int s = 0; s < p.nsteps; ++s) segs += p.steps[s].nseg;
+    if (segs > maxsegs) maxsegs = segs;
+  }
+  out->plan_bytes = (int)rbx::plan_smem_bytes(maxsegs);
   RBX_CUDA(cudaMalloc(reinterpret_cast<void**>(&out->dev), sizeof(rbx::Plan) * host.size()));
   RBX_CUDA(cudaMemcpy(out->dev, host.data(), sizeof(rbx::Plan) * host.size(), cudaMemcpyHostToDevice));
   out->nplans = (int)host.size();
@@ -193,12 +207,14 @@ int launch(rbx_comm* c, const CachedPlan& cp, int dtype, cudaStream_t stream, bo
   a.nblocks = nblocks;
   a.timeout_ns = c->timeout_ns;
   a.err = c->err_dev;
+  a.plan_bytes = cp.plan_bytes;
   void* params[] = {&a};
   dim3 grid((unsigned)(nblocks * cp.nplans)), block((unsigned)c->threads);
+  const size_t smem = (size_t)((cp.plan_bytes + 15) / 16 * 16);
   if (cooperative) {
-    RBX_CUDA(cudaLaunchCooperativeKernel(fn, grid, block, params, 0, stream));
+    RBX_CUDA(cudaLaunchCooperativeKernel(fn, grid, block, params, smem, stream));
   } else {
-    RBX_CUDA(cudaLaunchKernel(fn, grid, block, params, 0, stream));
+    RBX_CUDA(cudaLaunchKernel(fn, grid, block, params, smem, stream));
   }
   c->launches++;
   return RBX_OK;

@@ -18,6 +18,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdint.h>
 
 #include "rbx_plan.h"
@@ -318,6 +319,7 @@ struct ErrRecord {  // host-mapped; first failure wins
 struct KernelArgs {
   const Plan* plans;     // one per rank hosted by this launch
   int nblocks;           // CTAs per rank
+  int plan_bytes;        // bytes of each Plan staged in shared memory
   uint64_t timeout_ns;
   ErrRecord* err;
 };
@@ -338,21 +340,100 @@ __device__ __forceinline__ bool spin_flag(const uint32_t* f, uint32_t e, volatil
   return true;
 }
 
+// Bytes of a Plan that a launch needs in shared memory: everything up to the
+// segment array plus the segments actually used.
+__host__ __device__ inline size_t plan_smem_bytes(int nsegs) {
+  return offsetof(Plan, segs) + (size_t)nsegs * sizeof(Seg);
+}
+
+// Work of one step for CTA b: the step's body vectors (all segments
+// concatenated) are cut into tiles of `tile` vectors dealt round-robin to the
+// CTAs (tile == 0: one contiguous range per CTA).
+template <typename T>
+__device__ __forceinline__ void run_step_work(const Plan& P, const Step& st, int b, int nb, SegCtx& s_seg,
+                                              int& s_cur) {
+  const int64_t T_vec = st.total_vec;
+  auto setup = [&](int k) {
+    const Seg& sg = P.segs[st.seg0 + k];
+    __syncthreads();  // s_seg reuse
+    if (threadIdx.x < sg.nsrc) {
+      s_seg.src[threadIdx.x] = (const char*)P.ptrs[sg.tbl + sg.src[threadIdx.x]];
+      s_seg.ctrl[threadIdx.x] = sg.ctrl[threadIdx.x];
+    }
+    if (threadIdx.x < sg.ndst) s_seg.dst[threadIdx.x] = (char*)P.ptrs[sg.tbl + sg.dst[threadIdx.x]];
+    if (threadIdx.x == 0) {
+      s_seg.ndst = sg.ndst;
+      s_seg.nlev = sg.nlev;
+    }
+    __syncthreads();
+  };
+  auto body = [&](int64_t lo, int64_t hi) {  // [lo, hi) in step vector space
+    int k = 0;
+    while (k < st.nseg) {
+      const Seg& sg = P.segs[st.seg0 + k];
+      const int64_t a = lo > sg.vec_begin ? lo : sg.vec_begin;
+      const int64_t z = hi < sg.vec_begin + sg.nvec ? hi : sg.vec_begin + sg.nvec;
+      if (sg.vec_begin >= hi) break;
+      if (a < z) {
+        if (s_cur != k) {
+          setup(k);
+          s_cur = k;
+        }
+        dispatch_body<T>(sg.nsrc, sg.nlev, s_seg, sg.body_off, a - sg.vec_begin, z - sg.vec_begin);
+      }
+      ++k;
+    }
+  };
+  if (P.tile <= 0) {
+    const int64_t my0 = T_vec * b / nb, my1 = T_vec * (b + 1) / nb;
+    if (my0 < my1) body(my0, my1);
+  } else {
+    const int64_t tile = P.tile;
+    for (int64_t t = b; t * tile < T_vec; t += nb) {
+      const int64_t lo = t * tile;
+      body(lo, lo + tile < T_vec ? lo + tile : T_vec);
+    }
+  }
+  for (int k = b % nb; k < st.nseg; k += nb) {  // scalar head/tail of segment k: CTA k mod nb
+    const Seg& sg = P.segs[st.seg0 + k];
+    if (sg.head + sg.tail == 0) continue;
+    if (s_cur != k) {
+      setup(k);
+      s_cur = k;
+    }
+    for (int i = threadIdx.x; i < sg.head + sg.tail; i += blockDim.x) {
+      const int64_t elem = i < sg.head ? sg.off + i : sg.body_off + sg.nvec * P.vec + (i - sg.head);
+      dispatch_scalar<T>(sg.nsrc, sg.nlev, s_seg, elem);
+    }
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(512, 1) rbx_step_kernel(KernelArgs args) {
+  extern __shared__ __align__(16) unsigned char s_plan_raw[];
   const int vrank = blockIdx.x / args.nblocks;
   const int b = blockIdx.x % args.nblocks;
-  const Plan& P = args.plans[vrank];
   const int nb = args.nblocks;
   __shared__ uint32_t s_epoch;
   __shared__ int s_fail;
+  __shared__ int s_cur;
   __shared__ SegCtx s_seg;
+  {  // stage this rank's plan in shared memory (one coalesced copy instead of
+     // chains of dependent global loads on the critical path of every step)
+    const int4* src = reinterpret_cast<const int4*>(args.plans + vrank);
+    int4* dst = reinterpret_cast<int4*>(s_plan_raw);
+    const int words = (int)((args.plan_bytes + 15) / 16);
+    for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  const Plan& P = *reinterpret_cast<const Plan*>(s_plan_raw);
+  __syncthreads();
   uint32_t* my_sig = P.my_sig;
   volatile uint32_t* abort_word = my_sig ? (volatile uint32_t*)(my_sig + SigLayout::abort_off) : nullptr;
   const uint64_t t0 = P.nosync ? 0 : global_ns();
 
   if (threadIdx.x == 0) {
     s_fail = 0;
+    s_cur = -1;
     s_epoch = P.nosync ? 0u : my_sig[SigLayout::epoch_off + b] + 1u;
   }
   __syncthreads();
@@ -391,32 +472,9 @@ __global__ void __launch_bounds__(512, 1) rbx_step_kernel(KernelArgs args) {
       if (s_fail) return;
     }
     // ---- work ----
-    const int64_t T_vec = st.total_vec;
-    const int64_t my0 = T_vec * b / nb, my1 = T_vec * (b + 1) / nb;
-    for (int k = 0; k < st.nseg; ++k) {
-      const Seg& sg = P.segs[st.seg0 + k];
-      const bool scalar_part = (sg.head + sg.tail) > 0 && (k % nb) == b;
-      const int64_t lo = my0 > sg.vec_begin ? my0 : sg.vec_begin;
-      const int64_t hi = my1 < sg.vec_begin + sg.nvec ? my1 : sg.vec_begin + sg.nvec;
-      if (!(lo < hi) && !scalar_part) continue;
-      __syncthreads();  // s_seg reuse
-      if (threadIdx.x < sg.nsrc) {
-        s_seg.src[threadIdx.x] = (const char*)P.ptrs[sg.tbl + sg.src[threadIdx.x]];
-        s_seg.ctrl[threadIdx.x] = sg.ctrl[threadIdx.x];
-      }
-      if (threadIdx.x < sg.ndst) s_seg.dst[threadIdx.x] = (char*)P.ptrs[sg.tbl + sg.dst[threadIdx.x]];
-      if (threadIdx.x == 0) {
-        s_seg.ndst = sg.ndst;
-        s_seg.nlev = sg.nlev;
-      }
-      __syncthreads();
-      if (lo < hi) dispatch_body<T>(sg.nsrc, sg.nlev, s_seg, sg.body_off, lo - sg.vec_begin, hi - sg.vec_begin);
-      if (scalar_part) {
-        for (int i = threadIdx.x; i < sg.head + sg.tail; i += blockDim.x) {
-          const int64_t elem = i < sg.head ? sg.off + i : sg.body_off + sg.nvec * P.vec + (i - sg.head);
-          dispatch_scalar<T>(sg.nsrc, sg.nlev, s_seg, elem);
-        }
-      }
+    if (st.nseg) {
+      if (threadIdx.x == 0) s_cur = -1;
+      run_step_work<T>(P, st, b, nb, s_seg, s_cur);
     }
     // ---- signal ----
     if (!P.nosync && st.nsig) {

@@ -63,7 +63,7 @@ struct Step {
 struct Plan {
   int32_t me, nranks, nsteps, nentry;
   int32_t nosync, vec;     // vec = elements per 16-byte vector for this dtype
-  int32_t nblocks, pad;
+  int32_t nblocks, tile;   // tile: vectors per round-robin work tile (0 = one contiguous range per CTA)
   uint8_t entry_peers[RBX_MAX_RANKS];
   uint32_t* sig[RBX_MAX_RANKS];   // signal area of every rank (mapped)
   uint32_t* my_sig;               // == sig[me]
