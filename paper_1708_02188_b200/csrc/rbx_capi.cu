@@ -12,6 +12,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -97,7 +98,9 @@ struct rbx_comm {
   bool connected = false;
   int sm_count = 148;
   int max_coresident = 0;  // co-resident CTAs of the step kernel
-  int tile = 0;            // work tile in 16-byte vectors (0: contiguous range per CTA); env RBX_TILE
+  int tile = 1024;         // work tile in 16-byte vectors (0: contiguous range per CTA); env RBX_TILE
+  size_t bytes_per_cta = 512 * 1024;  // adaptive CTA count per call; env RBX_BYTES_PER_CTA
+  int min_blocks = 8;                 // env RBX_MIN_BLOCKS
 };
 
 namespace {
@@ -160,6 +163,8 @@ int common_init(rbx_comm* c, const int* dims, int ndims, int device, int threads
   c->threads = threads;
   c->device = device;
   if (const char* t = std::getenv("RBX_TILE")) c->tile = std::atoi(t);
+  if (const char* t = std::getenv("RBX_BYTES_PER_CTA")) c->bytes_per_cta = (size_t)std::max(1L, std::atol(t));
+  if (const char* t = std::getenv("RBX_MIN_BLOCKS")) c->min_blocks = std::max(1, std::atoi(t));
   RBX_CUDA(cudaSetDevice(device));
   RBX_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
   int rc = coresident_blocks(device, threads, &c->max_coresident);
@@ -310,7 +315,18 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
     if (rc) return rc;
     it = c->plans.emplace(key, cp).first;
   }
-  return launch(c, it->second, dtype, stream, false, c->nblocks);
+  // CTAs per call: enough to cover the bytes (bandwidth), few for small
+  // messages (each CTA costs flag traffic and launch spread).  Every rank
+  // derives the same value from the same counts.
+  int nb = c->nblocks;
+  if (op == RBX_OP_BARRIER) {
+    nb = c->min_blocks;
+  } else {
+    const int64_t want = (int64_t)((total * (size_t)es + c->bytes_per_cta - 1) / c->bytes_per_cta);
+    if (want < nb) nb = (int)(want < c->min_blocks ? c->min_blocks : want);
+  }
+  if (nb > c->nblocks) nb = c->nblocks;
+  return launch(c, it->second, dtype, stream, false, nb);
 }
 
 }  // namespace

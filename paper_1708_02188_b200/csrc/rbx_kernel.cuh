@@ -434,7 +434,9 @@ __global__ void __launch_bounds__(512, 1) rbx_step_kernel(KernelArgs args) {
   if (threadIdx.x == 0) {
     s_fail = 0;
     s_cur = -1;
-    s_epoch = P.nosync ? 0u : my_sig[SigLayout::epoch_off + b] + 1u;
+    // one epoch per rank (all CTAs of a launch agree; launches on a stream are
+    // ordered, so the previous launch's final increment is visible here)
+    s_epoch = P.nosync ? 0u : *(volatile uint32_t*)(my_sig + SigLayout::epoch_off) + 1u;
   }
   __syncthreads();
   const uint32_t e = s_epoch;
@@ -486,7 +488,18 @@ __global__ void __launch_bounds__(512, 1) rbx_step_kernel(KernelArgs args) {
       }
     }
   }
-  if (!P.nosync && threadIdx.x == 0) my_sig[SigLayout::epoch_off + b] = e;
+  if (!P.nosync) {  // the last CTA of this rank to finish publishes the new epoch
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned int* done = reinterpret_cast<unsigned int*>(my_sig + SigLayout::epoch_off + 1);
+      __threadfence();
+      if (atomicAdd(done, 1u) == (unsigned)nb - 1u) {
+        *done = 0u;
+        *(volatile uint32_t*)(my_sig + SigLayout::epoch_off) = e;
+        __threadfence();
+      }
+    }
+  }
 }
 
 }  // namespace rbx
