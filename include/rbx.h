@@ -93,6 +93,10 @@ int rbx_comm_connect(rbx_comm_t *comm, const rbx_ipc_handle_t *signal_handles);
 int rbx_comm_destroy(rbx_comm_t *comm);
 int rbx_comm_set_timeout(rbx_comm_t *comm, double seconds);
 int rbx_comm_info(rbx_comm_t *comm, int *rank, int *nranks, int *nblocks, int *threads, uint64_t *launches);
+/* Timeline of the last launch (RBX_TRACE=1 at create): %globaltimer ns of the first (words 0..31) and
+ * last (32..63) CTA: 0 start, 1 plan staged, 2 entry signalled, 3+3s/4+3s/5+3s step s waited/worked/
+ * signalled, 30 steps done, 31 exit.  Tracing / profiling subsystem. */
+int rbx_comm_trace(rbx_comm_t *comm, uint64_t *out, int cap);
 /* Collective registration: every rank passes its own (ptr, bytes) and all ranks' handles/offsets. */
 int rbx_register_buffer(rbx_comm_t *comm, void *ptr, size_t bytes, const rbx_ipc_handle_t *handles,
                         const uint64_t *offsets, int *buf_id);

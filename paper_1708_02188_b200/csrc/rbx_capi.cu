@@ -101,6 +101,7 @@ struct rbx_comm {
   int tile = 1024;         // work tile in 16-byte vectors (0: contiguous range per CTA); env RBX_TILE
   size_t bytes_per_cta = 512 * 1024;  // adaptive CTA count per call; env RBX_BYTES_PER_CTA
   int min_blocks = 8;                 // env RBX_MIN_BLOCKS
+  unsigned long long* trace_dev = nullptr;  // 64-word kernel timeline when RBX_TRACE is set
 };
 
 namespace {
@@ -169,6 +170,12 @@ int common_init(rbx_comm* c, const int* dims, int ndims, int device, int threads
   RBX_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
   int rc = coresident_blocks(device, threads, &c->max_coresident);
   if (rc) return rc;
+  if (const char* t = std::getenv("RBX_TRACE")) {
+    if (std::atoi(t)) {
+      RBX_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->trace_dev), 64 * sizeof(unsigned long long)));
+      RBX_CUDA(cudaMemset(c->trace_dev, 0, 64 * sizeof(unsigned long long)));
+    }
+  }
   RBX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(rbx::ErrRecord), cudaHostAllocMapped));
   std::memset(c->err_host, 0, sizeof(rbx::ErrRecord));
   RBX_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0));
@@ -213,6 +220,7 @@ int launch(rbx_comm* c, const CachedPlan& cp, int dtype, cudaStream_t stream, bo
   a.timeout_ns = c->timeout_ns;
   a.err = c->err_dev;
   a.plan_bytes = cp.plan_bytes;
+  a.trace = c->trace_dev;
   void* params[] = {&a};
   dim3 grid((unsigned)(nblocks * cp.nplans)), block((unsigned)c->threads);
   const size_t smem = (size_t)((cp.plan_bytes + 15) / 16 * 16);
@@ -505,6 +513,15 @@ int rbx_comm_destroy(rbx_comm_t* c) {
 int rbx_comm_set_timeout(rbx_comm_t* c, double seconds) {
   if (!c || seconds <= 0) return fail(RBX_ERR_INVALID, "timeout must be > 0");
   c->timeout_ns = (uint64_t)(seconds * 1e9);
+  return RBX_OK;
+}
+
+int rbx_comm_trace(rbx_comm_t* c, uint64_t* out, int cap) {
+  if (!c) return fail(RBX_ERR_INVALID, "null communicator");
+  if (!c->trace_dev) return fail(RBX_ERR_INVALID, "tracing is off (set RBX_TRACE=1 before creating the communicator)");
+  uint64_t buf[64];
+  RBX_CUDA(cudaMemcpy(buf, c->trace_dev, sizeof(buf), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < cap && i < 64; ++i) out[i] = buf[i];
   return RBX_OK;
 }
 

@@ -322,6 +322,7 @@ struct KernelArgs {
   int plan_bytes;        // bytes of each Plan staged in shared memory
   uint64_t timeout_ns;
   ErrRecord* err;
+  unsigned long long* trace;  // optional 64-word timeline (first/last CTA), or null
 };
 
 __device__ __forceinline__ bool flag_reached(uint32_t v, uint32_t e) { return (int32_t)(v - e) >= 0; }
@@ -351,7 +352,7 @@ __host__ __device__ inline size_t plan_smem_bytes(int nsegs) {
 // CTAs (tile == 0: one contiguous range per CTA).
 template <typename T>
 __device__ __forceinline__ void run_step_work(const Plan& P, const Step& st, int b, int nb, SegCtx& s_seg,
-                                              int& s_cur) {
+                                              int& s_cur /* thread-local: same value in every thread */) {
   const int64_t T_vec = st.total_vec;
   auto setup = [&](int k) {
     const Seg& sg = P.segs[st.seg0 + k];
@@ -416,8 +417,11 @@ __global__ void __launch_bounds__(512, 1) rbx_step_kernel(KernelArgs args) {
   const int nb = args.nblocks;
   __shared__ uint32_t s_epoch;
   __shared__ int s_fail;
-  __shared__ int s_cur;
   __shared__ SegCtx s_seg;
+  // optional timeline (RBX_TRACE): first and last CTA of the first rank
+  unsigned long long* tr = nullptr;
+  if (args.trace && threadIdx.x == 0 && vrank == 0 && (b == 0 || b == nb - 1)) tr = args.trace + (b == 0 ? 0 : 32);
+  if (tr) tr[0] = global_ns();
   {  // stage this rank's plan in shared memory (one coalesced copy instead of
      // chains of dependent global loads on the critical path of every step)
     const int4* src = reinterpret_cast<const int4*>(args.plans + vrank);
@@ -433,19 +437,20 @@ __global__ void __launch_bounds__(512, 1) rbx_step_kernel(KernelArgs args) {
 
   if (threadIdx.x == 0) {
     s_fail = 0;
-    s_cur = -1;
     // one epoch per rank (all CTAs of a launch agree; launches on a stream are
     // ordered, so the previous launch's final increment is visible here)
     s_epoch = P.nosync ? 0u : *(volatile uint32_t*)(my_sig + SigLayout::epoch_off) + 1u;
   }
   __syncthreads();
   const uint32_t e = s_epoch;
+  if (tr) tr[1] = global_ns();
 
   if (!P.nosync && threadIdx.x < P.nentry) {  // ENTRY: "my stream reached the collective"
     __threadfence_system();
     const int q = P.entry_peers[threadIdx.x];
     st_release_sys(P.sig[q] + flag_index(0, P.me, b), e);
   }
+  if (tr) tr[2] = global_ns();
 
   for (int s = 0; s < P.nsteps; ++s) {
     const Step& st = P.steps[s];
@@ -473,11 +478,13 @@ __global__ void __launch_bounds__(512, 1) rbx_step_kernel(KernelArgs args) {
       __syncthreads();
       if (s_fail) return;
     }
+    if (tr && s < 9) tr[3 + 3 * s] = global_ns();
     // ---- work ----
     if (st.nseg) {
-      if (threadIdx.x == 0) s_cur = -1;
-      run_step_work<T>(P, st, b, nb, s_seg, s_cur);
+      int cur = -1;  // segment whose pointers are in s_seg (thread-local, uniform)
+      run_step_work<T>(P, st, b, nb, s_seg, cur);
     }
+    if (tr && s < 9) tr[4 + 3 * s] = global_ns();
     // ---- signal ----
     if (!P.nosync && st.nsig) {
       __syncthreads();
@@ -487,7 +494,9 @@ __global__ void __launch_bounds__(512, 1) rbx_step_kernel(KernelArgs args) {
         st_release_sys(P.sig[q] + flag_index(s + 1, P.me, b), e);
       }
     }
+    if (tr && s < 9) tr[5 + 3 * s] = global_ns();
   }
+  if (tr) tr[30] = global_ns();
   if (!P.nosync) {  // the last CTA of this rank to finish publishes the new epoch
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -500,6 +509,7 @@ __global__ void __launch_bounds__(512, 1) rbx_step_kernel(KernelArgs args) {
       }
     }
   }
+  if (tr) tr[31] = global_ns();
 }
 
 }  // namespace rbx

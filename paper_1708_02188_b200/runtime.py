@@ -209,6 +209,24 @@ class RankContext:
         _native.check(self._L.rbx_comm_info(self._comm, None, None, ctypes.byref(nb), None, None))
         return nb.value
 
+    def trace(self) -> dict:
+        """Kernel timeline of the last launch (needs RBX_TRACE=1 before creation):
+        microseconds since the first CTA started, for the first and last CTA."""
+        buf = (ctypes.c_uint64 * 64)()
+        _native.check(self._L.rbx_comm_trace(self._comm, buf, 64))
+        t0 = buf[0]
+        names = {0: "start", 1: "plan_staged", 2: "entry_signalled", 30: "steps_done", 31: "exit"}
+        out = {}
+        for cta, base in (("first", 0), ("last", 32)):
+            row = {}
+            for i in range(32):
+                v = buf[base + i]
+                if v:
+                    nm = names.get(i) or f"step{(i - 3) // 3}_{('waited', 'worked', 'signalled')[(i - 3) % 3]}"
+                    row[nm] = round((v - t0) / 1e3, 3)
+            out[cta] = row
+        return out
+
     def schedule_for(self, element_count: int):
         return multiring_schedule(self.grid, element_count)
 
