@@ -107,7 +107,7 @@ int main() {
   for (int g : grids) {
     char nm[64];
     std::snprintf(nm, 64, "copy grid=%d", g);
-    timeit([&] { copyk<<<g, 512>>>(P.b[1], P.b[0], nvec * 4); }, 2.0 * 4 * n * 4, nm);
+    timeit([&] { copyk<<<g, 512>>>(P.b[1], P.b[0], nvec); }, 2.0 * n * 4, nm);
   }
   for (int g : grids) {
     char nm[64];
