@@ -99,8 +99,9 @@ struct rbx_comm {
   int sm_count = 148;
   int max_coresident = 0;  // co-resident CTAs of the step kernel
   int tile = 1024;         // work tile in 16-byte vectors (0: contiguous range per CTA); env RBX_TILE
-  size_t bytes_per_cta = 512 * 1024;  // adaptive CTA count per call; env RBX_BYTES_PER_CTA
-  int min_blocks = 8;                 // env RBX_MIN_BLOCKS
+  int local_tile = 512;    // same for the HBM-bound local mode (one block-iteration: grid-stride); env RBX_LOCAL_TILE
+  size_t bytes_per_cta = 32 * 1024;   // adaptive CTA count per call; env RBX_BYTES_PER_CTA
+  int min_blocks = 16;                // env RBX_MIN_BLOCKS
   unsigned long long* trace_dev = nullptr;  // 64-word kernel timeline when RBX_TRACE is set
 };
 
@@ -164,6 +165,7 @@ int common_init(rbx_comm* c, const int* dims, int ndims, int device, int threads
   c->threads = threads;
   c->device = device;
   if (const char* t = std::getenv("RBX_TILE")) c->tile = std::atoi(t);
+  if (const char* t = std::getenv("RBX_LOCAL_TILE")) c->local_tile = std::atoi(t);
   if (const char* t = std::getenv("RBX_BYTES_PER_CTA")) c->bytes_per_cta = (size_t)std::max(1L, std::atol(t));
   if (const char* t = std::getenv("RBX_MIN_BLOCKS")) c->min_blocks = std::max(1, std::atoi(t));
   RBX_CUDA(cudaSetDevice(device));
@@ -199,7 +201,7 @@ int upload(rbx_comm* c, std::vector<rbx::Plan>& host, const std::vector<void*>& 
   int maxsegs = 0;
   for (auto& p : host) {
     p.ptrs = out->ptrs;
-    p.tile = c->tile;
+    p.tile = p.nosync ? c->local_tile : c->tile;
     int segs = 0;
     for (int s = 0; s < p.nsteps; ++s) segs += p.steps[s].nseg;
     if (segs > maxsegs) maxsegs = segs;
