@@ -147,8 +147,9 @@ int coresident_blocks(int device, int threads, int* out) {
   RBX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   int worst = 1 << 30;
   const size_t max_smem = (rbx::plan_smem_bytes(RBX_MAX_SEGS) + 15) / 16 * 16;
+  static_assert((rbx::plan_smem_bytes(RBX_MAX_SEGS) + 15) / 16 * 16 + 1024 <= 48 * 1024,
+                "staged plan must fit the default dynamic shared memory window");
   for (int dt = RBX_F32; dt <= RBX_I32; ++dt) {
-    RBX_CUDA(cudaFuncSetAttribute(kernel_for(dt), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem));
     int per_sm = 0;
     RBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_for(dt), threads, max_smem));
     if (per_sm * sms < worst) worst = per_sm * sms;

@@ -353,7 +353,7 @@ __device__ __forceinline__ bool spin_flag(const uint32_t* f, uint32_t e, volatil
 
 // Bytes of a Plan that a launch needs in shared memory: everything up to the
 // segment array plus the segments actually used.
-__host__ __device__ inline size_t plan_smem_bytes(int nsegs) {
+__host__ __device__ constexpr size_t plan_smem_bytes(int nsegs) {
   return offsetof(Plan, segs) + (size_t)nsegs * sizeof(Seg);
 }
 
@@ -431,7 +431,10 @@ __global__ void __launch_bounds__(512, 1) rbx_step_kernel(KernelArgs args) {
   // optional timeline (RBX_TRACE): first and last CTA of the first rank
   unsigned long long* tr = nullptr;
   if (args.trace && threadIdx.x == 0 && vrank == 0 && (b == 0 || b == nb - 1)) tr = args.trace + (b == 0 ? 0 : 32);
-  if (tr) tr[0] = global_ns();
+  if (tr) {
+    tr[29] = tr[31];  // previous launch's exit on this comm: start - prev exit = launch gap
+    tr[0] = global_ns();
+  }
   {  // stage this rank's plan in shared memory (one coalesced copy instead of
      // chains of dependent global loads on the critical path of every step)
     const int4* src = reinterpret_cast<const int4*>(args.plans + vrank);

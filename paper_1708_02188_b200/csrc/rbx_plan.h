@@ -24,7 +24,7 @@
 #define RBX_MAX_RANKS 16
 #define RBX_MAX_LEVELS 4       // non-singleton grid dims (N <= 16 -> at most 4)
 #define RBX_MAX_STEPS 12
-#define RBX_MAX_SEGS 512
+#define RBX_MAX_SEGS 384       // keeps a staged plan under the 48 KB default shared-memory window
 #define RBX_MAX_WAITS 256
 #define RBX_MAX_SIGS 256
 #define RBX_MAX_BLOCKS 1024    // blocks per rank (flag array width)

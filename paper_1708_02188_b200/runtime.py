@@ -216,12 +216,12 @@ class RankContext:
         _native.check(self._L.rbx_comm_trace(self._comm, buf, 64))
         t0 = buf[0]
         names = {0: "start", 1: "plan_staged", 2: "entry_signalled", 30: "steps_done", 31: "exit"}
-        out = {}
+        out = {"gap_from_previous_launch_us": round((buf[0] - buf[29]) / 1e3, 3) if buf[29] else None}
         for cta, base in (("first", 0), ("last", 32)):
             row = {}
             for i in range(32):
                 v = buf[base + i]
-                if v:
+                if v and i != 29:
                     nm = names.get(i) or f"step{(i - 3) // 3}_{('waited', 'worked', 'signalled')[(i - 3) % 3]}"
                     row[nm] = round((v - t0) / 1e3, 3)
             out[cta] = row
