@@ -170,8 +170,13 @@ def flush_l2(scratch):
     """Evict L2: write a 256 MiB buffer (> 126 MB L2), then read it back so the
     dirty lines are written back before the timed region starts (otherwise
     their write-back would be charged to the kernel being timed)."""
+    import torch
+
     scratch.fill_(1.0)
     scratch.sum()
+    # ~50 us of device spin so the host enqueues the timed launch before the GPU
+    # gets there: the events then time the kernel, not Python launch latency
+    torch.cuda._sleep(100_000)
 
 
 def busbw(ranks: int, nbytes: int, seconds: float) -> float:

@@ -99,7 +99,7 @@ struct rbx_comm {
   int sm_count = 148;
   int max_coresident = 0;  // co-resident CTAs of the step kernel
   int tile = 1024;         // work tile in 16-byte vectors (0: contiguous range per CTA); env RBX_TILE
-  int local_tile = 512;    // same for the HBM-bound local mode (one block-iteration: grid-stride); env RBX_LOCAL_TILE
+  int local_tile = 2048;   // same for the HBM-bound local mode (measured best of 0/512/2048/4096/8192/32768); env RBX_LOCAL_TILE
   size_t bytes_per_cta = 32 * 1024;   // adaptive CTA count per call; env RBX_BYTES_PER_CTA
   int min_blocks = 16;                // env RBX_MIN_BLOCKS
   unsigned long long* trace_dev = nullptr;  // 64-word kernel timeline when RBX_TRACE is set

@@ -56,6 +56,7 @@ def main():
                     work.copy_(pristine)
                     scratch.fill_(1.0)
                     scratch.sum()
+                    torch.cuda._sleep(100_000)  # host runs ahead: events time the kernel, not launch latency
                     if impl == "ours":
                         ctx.barrier()
                     else:

@@ -48,6 +48,8 @@ def main():
                     for it in range(args.iters + 3):
                         if args.flush:
                             scratch.fill_(1.0)
+                            scratch.sum()
+                        torch.cuda._sleep(100_000)
                         ctx.barrier()
                         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                         s.record(stream)
