@@ -145,6 +145,16 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// 16-byte streaming load that bypasses L1 (peer data may change between
+// steps).  `volatile` keeps every load of a batch ahead of the arithmetic that
+// consumes it: ptxas otherwise interleaves them in pairs to save registers,
+// halving the bytes in flight (Little's law on HBM/NVLink latency).
+__device__ __forceinline__ int4 ld_stream(const char* p) {
+  int4 v;
+  asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -215,7 +225,7 @@ __device__ __noinline__ void fold_body(const SegCtx& sc, int64_t body_off, int64
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t idx = v + (int64_t)u * blockDim.x;
-        if (idx < v1) raw[u] = __ldcg(reinterpret_cast<const int4*>(p + idx * 16));
+        if (idx < v1) raw[u] = ld_stream(p + idx * 16);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -239,7 +249,7 @@ __device__ __noinline__ void fold_body(const SegCtx& sc, int64_t body_off, int64
           for (int k = 0; k < B; ++k)
             if (j0 + k < NSRC) {
               const char* p = NSRC > 8 ? ((const char* volatile*)sc.src)[j0 + k] : sc.src[j0 + k];
-              raw[u][k] = __ldcg(reinterpret_cast<const int4*>(p + base + idx * 16));
+              raw[u][k] = ld_stream(p + base + idx * 16);
             }
         }
       }
