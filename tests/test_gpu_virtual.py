@@ -180,6 +180,41 @@ def test_repeated_calls_epochs_and_launch_count():
     vr.close()
 
 
+@pytest.mark.parametrize("mode", ["local", "fused"])
+def test_cuda_graph_replay(mode):
+    """Epochs live in device memory, so a captured launch replays correctly
+    (CUDA graphs instead of per-call launches for static buffers)."""
+    torch = _torch()
+    from paper_1708_02188_b200.virtual import VirtualRanks
+
+    dims = (2, 2, 2)
+    grid = orc.Grid(dims)
+    length = 50_001
+    parts = [orc.generate_input(4, 0, r, length, "f32") for r in range(8)]
+    want = orc.closed_form_allreduce(grid, parts)
+    vr = VirtualRanks(dims, nblocks_per_rank=0 if mode == "local" else 4)
+    src = [torch.from_numpy(p.copy()).cuda() for p in parts]
+    ts = [s.clone() for s in src]
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        vr.collective(ts, mode=mode, stream=s)  # warm-up: builds and uploads the plan
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        vr.collective(ts, mode=mode, stream=torch.cuda.current_stream())
+    for _ in range(3):
+        for t, x in zip(ts, src):
+            t.copy_(x)
+        g.replay()
+        torch.cuda.synchronize()
+        vr.check()
+        for t in ts:
+            assert np.array_equal(t.cpu().numpy(), want)
+    vr.close()
+
+
 @pytest.mark.parametrize("mode", ["local", "fused", "ring_dims"])
 def test_windows_compose_to_the_full_allreduce(mode):
     """rbx_vcollective_window: element windows keep the full buffer's chunk
