@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--batch", type=int, default=32)  # per GPU
     ap.add_argument("--amp", default="bf16", choices=["bf16", "none"])
+    ap.add_argument("--nblocks", type=int, default=32, help="CTAs of the allreduce kernel (leave SMs to backward)")
+    ap.add_argument("--bucket-view", type=int, default=1, help="gradient_as_bucket_view")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -46,7 +48,8 @@ def main():
     hook_state = None
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-        model = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local], bucket_cap_mb=25)
+        model = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local], bucket_cap_mb=25,
+                                                          gradient_as_bucket_view=bool(args.bucket_view))
         if args.comm == "ours":
             from paper_1708_02188_b200.ddp import MultiringHookState, multiring_allreduce_hook
             from paper_1708_02188_b200.multiring import Grid
@@ -54,7 +57,7 @@ def main():
 
             dims = {2: (2,), 4: (2, 2), 8: (2, 2, 2)}.get(world, (world,))
             gloo = dist.new_group(backend="gloo")  # host plumbing for handle exchange
-            ctx = RankContext(rank, Grid(dims), group=gloo, device=local, blocking=False)
+            ctx = RankContext(rank, Grid(dims), group=gloo, device=local, nblocks=args.nblocks, blocking=False)
             hook_state = MultiringHookState(ctx)
             model.register_comm_hook(hook_state, multiring_allreduce_hook)
     opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9)
@@ -92,6 +95,7 @@ def main():
         print(json.dumps({
             "config": "config5: ResNet-50 DDP step, synthetic 3x224x224, 1000 classes",
             "comm": args.comm if world > 1 else "none", "n_gpus": world, "batch_per_gpu": args.batch,
+            "nblocks": args.nblocks if args.comm == "ours" else None, "bucket_view": bool(args.bucket_view),
             "amp": args.amp, "params": nparams, "grad_bytes": nparams * 4,
             "t_iter_ms": round(t_ms, 3), "images_per_s": round(world * args.batch / t_ms * 1e3, 1),
             "loss": float(loss.item()),
