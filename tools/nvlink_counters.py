@@ -43,6 +43,29 @@ def nvml_counters(handle, pynvml):
     return tuple(out)
 
 
+def smi_counters(index: int):
+    """Fallback: `nvidia-smi nvlink -gt d` per-link Data Tx/Rx counters (KiB)."""
+    import re
+    import subprocess
+
+    try:
+        txt = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", str(index)], capture_output=True, text=True,
+                             timeout=30).stdout
+    except Exception:
+        return None, ""
+    tx = rx = 0
+    seen = False
+    for line in txt.splitlines():
+        m = re.search(r"Data (Tx|Rx):\s*([0-9]+)\s*KiB", line)
+        if m:
+            seen = True
+            if m.group(1) == "Tx":
+                tx += int(m.group(2)) * 1024
+            else:
+                rx += int(m.group(2)) * 1024
+    return ((tx, rx) if seen else None), txt
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--elems", type=int, default=25_600_000)
@@ -74,8 +97,14 @@ def main():
     dist.barrier()
     time.sleep(0.5)
     c0 = nvml_counters(h, pynvml)
+    src = "nvml"
+    raw0 = ""
+    if c0 is None:
+        c0, raw0 = smi_counters(rank)
+        src = "nvidia-smi nvlink -gt d"
     ts = []
     for _ in range(args.iters):
+        ctx.barrier()  # align ranks so kernel_us is the collective, not the skew
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record(stream)
         ctx.collective("allreduce", work, mode=args.mode)
@@ -85,7 +114,7 @@ def main():
     torch.cuda.synchronize()
     dist.barrier()
     time.sleep(0.5)
-    c1 = nvml_counters(h, pynvml)
+    c1 = nvml_counters(h, pynvml) if src == "nvml" else smi_counters(rank)[0]
     kt = sum(s.elapsed_time(e) for s, e in ts) / len(ts) / 1e3
     S = args.elems * 4
     alg = 2 * (world - 1) / world * S
@@ -99,6 +128,8 @@ def main():
                     "achieved_tx_gbs": round(tx / kt / 1e9, 1), "achieved_rx_gbs": round(rx / kt / 1e9, 1)})
     else:
         row["nvml"] = "NVLink throughput fields unavailable"
+        row["smi_raw_head"] = raw0[:600]
+    row["counter_source"] = src
     rows = [None] * world
     dist.all_gather_object(rows, row)
     if rank == 0:
