@@ -14,7 +14,7 @@ import os
 from .errors import CollectiveError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librbx.so")
+LIB_PATH = os.environ.get("RBX_LIB_PATH") or os.path.join(_HERE, "librbx.so")  # override: A/B builds only
 
 OK, ERR_INVALID, ERR_CUDA, ERR_COLLECTIVE, ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 DTYPE_CODES = {"f32": 0, "f64": 1, "i64": 2, "bf16": 3, "f16": 4, "i32": 5}

@@ -213,7 +213,10 @@ template <typename T, int NSRC, int NLEV>
 __device__ __noinline__ void fold_body(const SegCtx& sc, int64_t body_off, int64_t v0, int64_t v1) {
   constexpr int VEC = Traits<T>::VEC;
   constexpr int B = NSRC < 8 ? NSRC : 8;  // operands per load batch
-  constexpr int U_LD = 8 / B > 0 ? 8 / B : 1;
+#ifndef RBX_LD_DEPTH
+#define RBX_LD_DEPTH 16  // 16-byte loads in flight per thread (per batch)
+#endif
+  constexpr int U_LD = RBX_LD_DEPTH / B > 0 ? RBX_LD_DEPTH / B : 1;
   constexpr int U_ACC = 32 / (NLEV * VEC) > 0 ? 32 / (NLEV * VEC) : 1;
   constexpr int U = NSRC == 1 ? 8 : (U_LD < U_ACC ? U_LD : U_ACC);
   const int64_t base = body_off * (int64_t)sizeof(T);
