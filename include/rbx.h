@@ -78,6 +78,9 @@ int64_t rbx_plan_describe(const int *dims, int ndims, int rank, int64_t count, i
 
 /* ---- devices and symmetric memory ---- */
 int rbx_device_count(int *n);
+/* Single-process use of several GPUs (virtual ranks on distinct devices, profiling harnesses):
+ * lets `device` load/store `peer`'s memory directly over NVLink. */
+int rbx_enable_peer_access(int device, int peer);
 /* PlacedBuffer(memory="device") storage (runtime.py:51-69): cudaMalloc + IPC export. */
 int rbx_alloc_symmetric(int device, size_t bytes, void **ptr, rbx_ipc_handle_t *handle);
 int rbx_free(void *ptr);

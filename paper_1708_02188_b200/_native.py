@@ -64,6 +64,7 @@ def lib() -> ctypes.CDLL:
     _sig(L.rbx_fold_order, c_int, _INTP, c_int, c_int, _INTP)
     _sig(L.rbx_plan_describe, c_i64, _INTP, c_int, c_int, c_i64, c_int, c_int, c_int, _I64P, c_i64)
     _sig(L.rbx_device_count, c_int, _INTP)
+    _sig(L.rbx_enable_peer_access, c_int, c_int, c_int)
     _sig(L.rbx_alloc_symmetric, c_int, c_int, c_size, ctypes.POINTER(_VP), HP)
     _sig(L.rbx_free, c_int, _VP)
     _sig(L.rbx_export_buffer, c_int, _VP, HP, ctypes.POINTER(ctypes.c_uint64))
@@ -92,7 +93,7 @@ def lib() -> ctypes.CDLL:
 
 EXPORTED = [
     "rbx_version", "rbx_last_error", "rbx_chunk_bounds", "rbx_owned_region", "rbx_fold_order", "rbx_plan_describe",
-    "rbx_device_count", "rbx_alloc_symmetric", "rbx_free", "rbx_export_buffer", "rbx_comm_create",
+    "rbx_device_count", "rbx_enable_peer_access", "rbx_alloc_symmetric", "rbx_free", "rbx_export_buffer", "rbx_comm_create",
     "rbx_comm_connect", "rbx_comm_destroy", "rbx_comm_set_timeout", "rbx_comm_info", "rbx_comm_trace",
     "rbx_register_buffer",
     "rbx_allreduce", "rbx_reduce_scatter", "rbx_allgather", "rbx_allreduce_buckets", "rbx_allreduce_window",

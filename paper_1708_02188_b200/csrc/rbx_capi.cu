@@ -407,6 +407,17 @@ int rbx_device_count(int* n) {
   return RBX_OK;
 }
 
+int rbx_enable_peer_access(int device, int peer) {
+  RBX_CUDA(cudaSetDevice(device));
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    (void)cudaGetLastError();
+    return RBX_OK;
+  }
+  RBX_CUDA(e);
+  return RBX_OK;
+}
+
 int rbx_alloc_symmetric(int device, size_t bytes, void** ptr, rbx_ipc_handle_t* handle) {
   RBX_CUDA(cudaSetDevice(device));
   RBX_CUDA(cudaMalloc(ptr, bytes ? bytes : 256));

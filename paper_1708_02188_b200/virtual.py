@@ -20,7 +20,10 @@ from .runtime import _dtype_name
 
 
 class VirtualRanks:
-    def __init__(self, dims, device: int = 0, nblocks_per_rank: int = 0, threads: int = 512, timeout_s: float = 30.0):
+    def __init__(self, dims, device: int = 0, nblocks_per_rank: int = 0, threads: int = 512, timeout_s: float = 30.0,
+                 peer_devices=()):
+        """peer_devices: other GPUs whose memory rank buffers may live in (the
+        single launch on `device` then reads/writes them over NVLink)."""
         import torch
 
         if not torch.cuda.is_available():
@@ -36,6 +39,10 @@ class VirtualRanks:
         _native.check(self._L.rbx_vcomm_create(ctypes.byref(self._comm), n, _native.ints(self.dims), len(self.dims),
                                                device, nblocks_per_rank, threads))
         self._L.rbx_comm_set_timeout(self._comm, float(timeout_s))
+        self.devices = {self.device.index}
+        for p in peer_devices:
+            _native.check(self._L.rbx_enable_peer_access(device, int(p)))
+            self.devices.add(int(p))
 
     @property
     def launches(self) -> int:
@@ -59,7 +66,7 @@ class VirtualRanks:
         n = tensors[0].numel()
         dt = _dtype_name(tensors[0])
         for t in tensors:
-            if t.numel() != n or _dtype_name(t) != dt or not t.is_contiguous() or t.device != self.device:
+            if t.numel() != n or _dtype_name(t) != dt or not t.is_contiguous() or t.device.index not in self.devices:
                 raise ValueError("virtual-rank buffers must match in length/dtype/device and be contiguous")
         ptrs = (ctypes.c_void_p * self.nranks)(*[t.data_ptr() for t in tensors])
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
