@@ -209,21 +209,8 @@ struct SegCtx {
 // 16-byte loads of a batch of up to 8 operands (x U independent vectors) are
 // all issued before any arithmetic, so every thread keeps ~8 NVLink/HBM
 // requests in flight; operands stay raw (int4) until folded.
-// The CTA's share of one segment: the step's body vectors are cut into tiles
-// of `tile` vectors dealt round-robin to the CTAs; this CTA handles the tiles
-// t = b (mod nb) that overlap the segment's vectors [begin, begin + nvec).
-struct Share {
-  int64_t begin, nvec, tile;
-  int b, nb;
-  __device__ __forceinline__ int64_t first_tile() const {
-    int64_t t = begin / tile;
-    return t + ((b - (int)(t % nb)) % nb + nb) % nb;
-  }
-  __device__ __forceinline__ bool any() const { return first_tile() * tile < begin + nvec; }
-};
-
 template <typename T, int NSRC, int NLEV>
-__device__ __forceinline__ void fold_range(const SegCtx& sc, int64_t body_off, int64_t v0, int64_t v1) {
+__device__ __noinline__ void fold_body(const SegCtx& sc, int64_t body_off, int64_t v0, int64_t v1) {
   constexpr int VEC = Traits<T>::VEC;
   constexpr int B = NSRC < 8 ? NSRC : 8;  // operands per load batch
 #ifndef RBX_LD_DEPTH
@@ -293,18 +280,6 @@ __device__ __forceinline__ void fold_range(const SegCtx& sc, int64_t body_off, i
   }
 }
 
-// One call per (segment, CTA): loops over all of the CTA's tiles inside, so the
-// noinline call/ABI cost is paid once per segment, not once per tile.
-template <typename T, int NSRC, int NLEV>
-__device__ __noinline__ void fold_body(const SegCtx& sc, int64_t body_off, Share sh) {
-  const int64_t end = sh.begin + sh.nvec;
-  for (int64_t t = sh.first_tile(); t * sh.tile < end; t += sh.nb) {
-    const int64_t lo = t * sh.tile > sh.begin ? t * sh.tile : sh.begin;
-    const int64_t hi = (t + 1) * sh.tile < end ? (t + 1) * sh.tile : end;
-    fold_range<T, NSRC, NLEV>(sc, body_off, lo - sh.begin, hi - sh.begin);
-  }
-}
-
 template <typename T, int NSRC, int NLEV>
 __device__ __forceinline__ void fold_scalar(const SegCtx& sc, int64_t elem) {
   using Tr = Traits<T>;
@@ -334,11 +309,12 @@ __device__ __forceinline__ void fold_scalar(const SegCtx& sc, int64_t elem) {
 #endif
 
 template <typename T>
-__device__ __forceinline__ void dispatch_body(int nsrc, int nlev, const SegCtx& sc, int64_t body_off, Share sh) {
+__device__ __forceinline__ void dispatch_body(int nsrc, int nlev, const SegCtx& sc, int64_t body_off, int64_t v0,
+                                              int64_t v1) {
   switch (nsrc * 8 + nlev) {
 #define RBX_CASE(N, L) \
   case N * 8 + L:      \
-    fold_body<T, N, L>(sc, body_off, sh); break;
+    fold_body<T, N, L>(sc, body_off, v0, v1); break;
     RBX_FOLD_SHAPES(RBX_CASE)
 #undef RBX_CASE
     default: break;
@@ -415,18 +391,32 @@ __device__ __forceinline__ void run_step_work(const Plan& P, const Step& st, int
     }
     __syncthreads();
   };
-  // tile 0 = one contiguous range per CTA
-  const int64_t tile = P.tile > 0 ? (int64_t)P.tile : (T_vec + nb - 1) / nb;
-  for (int k = 0; k < st.nseg; ++k) {
-    const Seg& sg = P.segs[st.seg0 + k];
-    if (sg.nvec == 0 || tile == 0) continue;
-    Share sh{sg.vec_begin, sg.nvec, tile, b, nb};
-    if (!sh.any()) continue;
-    if (s_cur != k) {
-      setup(k);
-      s_cur = k;
+  auto body = [&](int64_t lo, int64_t hi) {  // [lo, hi) in step vector space
+    int k = 0;
+    while (k < st.nseg) {
+      const Seg& sg = P.segs[st.seg0 + k];
+      const int64_t a = lo > sg.vec_begin ? lo : sg.vec_begin;
+      const int64_t z = hi < sg.vec_begin + sg.nvec ? hi : sg.vec_begin + sg.nvec;
+      if (sg.vec_begin >= hi) break;
+      if (a < z) {
+        if (s_cur != k) {
+          setup(k);
+          s_cur = k;
+        }
+        dispatch_body<T>(sg.nsrc, sg.nlev, s_seg, sg.body_off, a - sg.vec_begin, z - sg.vec_begin);
+      }
+      ++k;
     }
-    dispatch_body<T>(sg.nsrc, sg.nlev, s_seg, sg.body_off, sh);
+  };
+  if (P.tile <= 0) {
+    const int64_t my0 = T_vec * b / nb, my1 = T_vec * (b + 1) / nb;
+    if (my0 < my1) body(my0, my1);
+  } else {
+    const int64_t tile = P.tile;
+    for (int64_t t = b; t * tile < T_vec; t += nb) {
+      const int64_t lo = t * tile;
+      body(lo, lo + tile < T_vec ? lo + tile : T_vec);
+    }
   }
   for (int k = b % nb; k < st.nseg; k += nb) {  // scalar head/tail of segment k: CTA k mod nb
     const Seg& sg = P.segs[st.seg0 + k];
