@@ -47,6 +47,8 @@ extern "C" {
 #define RBX_MODE_FUSED 2      /* all dims folded in one pass (nested order), result pushed to every peer */
 #define RBX_MODE_FUSED_PULL 3 /* like FUSED, but the all-gather pulls the peers' owned chunks */
 #define RBX_MODE_LOCAL 4      /* virtual ranks on one GPU, no synchronisation (1-GPU roofline) */
+#define RBX_MODE_PUSH 5       /* two-shot, NVLink writes only: inputs pushed to the owners' inboxes
+                                 (rbx_set_inbox), results pushed back to every rank */
 
 /* collective ops */
 #define RBX_OP_ALLREDUCE 0
@@ -103,6 +105,12 @@ int rbx_comm_trace(rbx_comm_t *comm, uint64_t *out, int cap);
 /* Collective registration: every rank passes its own (ptr, bytes) and all ranks' handles/offsets. */
 int rbx_register_buffer(rbx_comm_t *comm, void *ptr, size_t bytes, const rbx_ipc_handle_t *handles,
                         const uint64_t *offsets, int *buf_id);
+
+/* MODE_PUSH scratch: bytes of symmetric inbox the given buffers need (host-only), and the collective
+ * registration of this rank's inbox (handles/offsets of every rank, like rbx_register_buffer). */
+int64_t rbx_inbox_bytes(const int *dims, int ndims, const size_t *counts, int nbufs, int dtype);
+int rbx_set_inbox(rbx_comm_t *comm, void *ptr, size_t bytes, const rbx_ipc_handle_t *handles,
+                  const uint64_t *offsets);
 
 /* ---- collectives (asynchronous on `stream`, a cudaStream_t or NULL) ---- */
 /* runtime.allreduce(ctx, obj) -- pkg/src/ringbox/runtime.py:295-297 */

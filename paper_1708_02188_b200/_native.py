@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("RBX_LIB_PATH") or os.path.join(_HERE, "librbx.so")  #
 OK, ERR_INVALID, ERR_CUDA, ERR_COLLECTIVE, ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 DTYPE_CODES = {"f32": 0, "f64": 1, "i64": 2, "bf16": 3, "f16": 4, "i32": 5}
 ITEMSIZE = {"f32": 4, "f64": 8, "i64": 8, "bf16": 2, "f16": 2, "i32": 4}
-MODES = {"auto": 0, "ring_dims": 1, "fused": 2, "fused_pull": 3, "local": 4}
+MODES = {"auto": 0, "ring_dims": 1, "fused": 2, "fused_pull": 3, "local": 4, "push": 5}
 OPS = {"allreduce": 0, "reduce_scatter": 1, "allgather": 2, "barrier": 3}
 
 
@@ -75,6 +75,8 @@ def lib() -> ctypes.CDLL:
     _sig(L.rbx_comm_info, c_int, _VP, _INTP, _INTP, _INTP, _INTP, ctypes.POINTER(ctypes.c_uint64))
     _sig(L.rbx_comm_trace, c_int, _VP, ctypes.POINTER(ctypes.c_uint64), c_int)
     _sig(L.rbx_register_buffer, c_int, _VP, _VP, c_size, HP, ctypes.POINTER(ctypes.c_uint64), _INTP)
+    _sig(L.rbx_inbox_bytes, c_i64, _INTP, c_int, ctypes.POINTER(c_size), c_int, c_int)
+    _sig(L.rbx_set_inbox, c_int, _VP, _VP, c_size, HP, ctypes.POINTER(ctypes.c_uint64))
     _sig(L.rbx_allreduce, c_int, _VP, _VP, c_size, c_int, c_int, _VP)
     _sig(L.rbx_reduce_scatter, c_int, _VP, _VP, c_size, c_int, c_int, _VP, _I64P, _I64P)
     _sig(L.rbx_allgather, c_int, _VP, _VP, c_size, c_int, c_int, _VP)
@@ -95,7 +97,7 @@ EXPORTED = [
     "rbx_version", "rbx_last_error", "rbx_chunk_bounds", "rbx_owned_region", "rbx_fold_order", "rbx_plan_describe",
     "rbx_device_count", "rbx_enable_peer_access", "rbx_alloc_symmetric", "rbx_free", "rbx_export_buffer", "rbx_comm_create",
     "rbx_comm_connect", "rbx_comm_destroy", "rbx_comm_set_timeout", "rbx_comm_info", "rbx_comm_trace",
-    "rbx_register_buffer",
+    "rbx_register_buffer", "rbx_inbox_bytes", "rbx_set_inbox",
     "rbx_allreduce", "rbx_reduce_scatter", "rbx_allgather", "rbx_allreduce_buckets", "rbx_allreduce_window",
     "rbx_barrier", "rbx_check", "rbx_vcomm_create", "rbx_vcollective", "rbx_vcollective_window",
 ]
@@ -150,6 +152,15 @@ def plan_describe(dims, rank: int, count: int, op: str = "allreduce", mode: str 
         check(ERR_INVALID)
     assert n <= cap
     return list(buf[:n])
+
+
+def inbox_bytes(dims, counts, dtype: str) -> int:
+    """Symmetric inbox bytes MODE_PUSH needs for these buffers (host-only)."""
+    cs = (ctypes.c_size_t * max(1, len(counts)))(*counts)
+    n = lib().rbx_inbox_bytes(ints(dims), len(dims), cs, len(counts), DTYPE_CODES[dtype])
+    if n < 0:
+        check(ERR_INVALID)
+    return n
 
 
 def parse_plan(words: list) -> dict:

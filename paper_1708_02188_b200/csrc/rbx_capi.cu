@@ -73,6 +73,7 @@ struct CachedPlan {
   void** ptrs = nullptr;
   int nplans = 0;
   int plan_bytes = 0;  // staged into shared memory by every CTA
+  bool uses_inbox = false;
 };
 
 struct OpenedHandle {
@@ -103,6 +104,11 @@ struct rbx_comm {
   size_t bytes_per_cta = 32 * 1024;   // adaptive CTA count per call; env RBX_BYTES_PER_CTA
   int min_blocks = 16;                // env RBX_MIN_BLOCKS
   unsigned long long* trace_dev = nullptr;  // 64-word kernel timeline when RBX_TRACE is set
+  // MODE_PUSH inboxes: this rank's (registered, symmetric) and every rank's mapping
+  char* inbox_local = nullptr;
+  size_t inbox_bytes = 0;
+  std::vector<char*> inbox_at;
+  bool inbox_owned = false;  // virtual comms allocate their own
 };
 
 namespace {
@@ -195,13 +201,23 @@ std::string plan_key(int op, int mode, int dtype, const std::vector<const void*>
   return k;
 }
 
-int upload(rbx_comm* c, std::vector<rbx::Plan>& host, const std::vector<void*>& ptrs, CachedPlan* out) {
-  RBX_CUDA(cudaMalloc(reinterpret_cast<void**>(&out->ptrs), sizeof(void*) * (ptrs.size() ? ptrs.size() : 1)));
-  if (!ptrs.empty())
-    RBX_CUDA(cudaMemcpy(out->ptrs, ptrs.data(), sizeof(void*) * ptrs.size(), cudaMemcpyHostToDevice));
+// tables: one pointer table shared by every plan, or one per plan (MODE_PUSH
+// tables depend on the rank: own inbox slots, this rank's slot in the peers').
+int upload(rbx_comm* c, std::vector<rbx::Plan>& host, const std::vector<std::vector<void*>>& tables,
+           CachedPlan* out) {
+  std::vector<void*> flat;
+  std::vector<size_t> base;
+  for (const auto& t : tables) {
+    base.push_back(flat.size());
+    flat.insert(flat.end(), t.begin(), t.end());
+  }
+  RBX_CUDA(cudaMalloc(reinterpret_cast<void**>(&out->ptrs), sizeof(void*) * (flat.size() ? flat.size() : 1)));
+  if (!flat.empty())
+    RBX_CUDA(cudaMemcpy(out->ptrs, flat.data(), sizeof(void*) * flat.size(), cudaMemcpyHostToDevice));
   int maxsegs = 0;
-  for (auto& p : host) {
-    p.ptrs = out->ptrs;
+  for (size_t i = 0; i < host.size(); ++i) {
+    rbx::Plan& p = host[i];
+    p.ptrs = out->ptrs + (tables.size() == host.size() ? base[i] : 0);
     p.tile = p.nosync ? c->local_tile : c->tile;
     int segs = 0;
     for (int s = 0; s < p.nsteps; ++s) segs += p.steps[s].nseg;
@@ -243,8 +259,33 @@ int check_mode_dtype(int mode, int dtype) {
   if (mode == RBX_MODE_RING_DIMS && (dtype == RBX_BF16 || dtype == RBX_F16))
     return fail(RBX_ERR_UNSUPPORTED, "MODE_RING_DIMS with bf16/f16 needs fp32 partial workspaces (not implemented); "
                                      "use MODE_FUSED, which folds in fp32 and rounds once");
-  if (mode < RBX_MODE_AUTO || mode > RBX_MODE_LOCAL) return fail(RBX_ERR_INVALID, "unknown mode");
+  if (mode < RBX_MODE_AUTO || mode > RBX_MODE_PUSH) return fail(RBX_ERR_INVALID, "unknown mode");
   return RBX_OK;
+}
+
+// MODE_PUSH pointer-table entries of rank `me` for one buffer (rbx_plan.h
+// table_entries): buffers, own inbox slots, own slot in every peer's inbox.
+// Inbox pointers are biased by -off*itemsize so the plan's element offsets
+// address them directly, and padded so that element `off` sits at the same
+// 16-byte phase as in the buffer (one head/body/tail split fits both).
+std::vector<void*> push_table(const rbx::Geometry& g, int me, int64_t count, int es, int mis,
+                              const std::vector<char*>& bufs, const std::vector<char*>& inbox, int64_t inbox_off) {
+  const int R = g.nranks;
+  const int m = (int)g.active_dims().size();
+  const int vec = 16 / es;
+  const int64_t slot = rbx::inbox_slot_bytes(g, count, es);
+  std::vector<void*> t(3 * R, nullptr);
+  for (int q = 0; q < R; ++q) t[q] = bufs[q];
+  auto biased = [&](int owner, int slot_idx) -> void* {
+    int64_t o, l;
+    rbx::region_after(g, owner, count, m, &o, &l);
+    const int64_t pad = mis >= 0 ? ((mis + o) % vec) * es : 0;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(inbox[owner]) + inbox_off + slot_idx * slot + pad - o * es;
+    return reinterpret_cast<void*>(a);
+  };
+  for (int p = 0; p < R; ++p) t[R + p] = biased(me, p);
+  for (int q = 0; q < R; ++q) t[2 * R + q] = biased(q, me);
+  return t;
 }
 
 // Elements between the previous 16-byte boundary and element 0, if identical
@@ -302,27 +343,43 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
     spec.nblocks = c->nblocks;
     spec.lo = lo;
     spec.hi = hi;
+    const bool push = mode == RBX_MODE_PUSH && (op == RBX_OP_ALLREDUCE || op == RBX_OP_REDUCE_SCATTER);
+    const int E = push ? 3 * c->nranks : c->nranks;  // pointer-table entries per buffer
+    int64_t inbox_off = 0;
     std::string err;
     for (int k = 0; k < nbufs; ++k) {
       int id;
       size_t off;
       if (op != RBX_OP_BARRIER && counts[k] == 0) {
-        for (int q = 0; q < c->nranks; ++q) ptrs.push_back(nullptr);  // empty bucket: never dereferenced
+        for (int q = 0; q < E; ++q) ptrs.push_back(nullptr);  // empty bucket: never dereferenced
       } else if (op != RBX_OP_BARRIER) {
         int rc = find_buffer(c, bufs[k], counts[k] * es, &id, &off);
         if (rc) return rc;
-        std::vector<void*> mine;
+        std::vector<char*> mine;
         for (int q = 0; q < c->nranks; ++q) mine.push_back(c->bufs[id].at[q] + off);
-        spec.mis = misalign(mine, es);
-        ptrs.insert(ptrs.end(), mine.begin(), mine.end());
+        spec.mis = misalign(std::vector<void*>(mine.begin(), mine.end()), es);
+        if (push) {
+          const int64_t need = rbx::inbox_buffer_bytes(c->geo, (int64_t)counts[k], es);
+          if (inbox_off + need > (int64_t)c->inbox_bytes)
+            return fail(RBX_ERR_INVALID, "MODE_PUSH inbox too small: need " + std::to_string(inbox_off + need) +
+                                             " bytes, have " + std::to_string(c->inbox_bytes) +
+                                             " (rbx_set_inbox; size with rbx_inbox_bytes)");
+          std::vector<void*> t = push_table(c->geo, c->rank, (int64_t)counts[k], es, spec.mis, mine, c->inbox_at,
+                                            inbox_off);
+          ptrs.insert(ptrs.end(), t.begin(), t.end());
+          inbox_off += need;
+        } else {
+          ptrs.insert(ptrs.end(), mine.begin(), mine.end());
+        }
       }
-      if (!rbx::build_plan(c->geo, c->rank, (int64_t)counts[k], spec, k * c->nranks, &host[0], k == 0, &err))
+      if (!rbx::build_plan(c->geo, c->rank, (int64_t)counts[k], spec, k * E, &host[0], k == 0, &err))
         return fail(RBX_ERR_INVALID, err);
     }
     for (int q = 0; q < c->nranks; ++q) host[0].sig[q] = c->sig[q];
     host[0].my_sig = c->sig[c->rank];
     CachedPlan cp;
-    int rc = upload(c, host, ptrs, &cp);
+    cp.uses_inbox = push;
+    int rc = upload(c, host, {ptrs}, &cp);
     if (rc) return rc;
     it = c->plans.emplace(key, cp).first;
   }
@@ -519,6 +576,7 @@ int rbx_comm_destroy(rbx_comm_t* c) {
     }
   }
   if (c->sig_local) cudaFree(c->sig_local);
+  if (c->inbox_owned && c->inbox_local) cudaFree(c->inbox_local);
   if (c->err_host) cudaFreeHost(c->err_host);
   delete c;
   return RBX_OK;
@@ -546,6 +604,49 @@ int rbx_comm_info(rbx_comm_t* c, int* rank, int* nranks, int* nblocks, int* thre
   if (nblocks) *nblocks = c->nblocks;
   if (threads) *threads = c->threads;
   if (launches) *launches = c->launches;
+  return RBX_OK;
+}
+
+int64_t rbx_inbox_bytes(const int* dims, int ndims, const size_t* counts, int nbufs, int dtype) {
+  rbx::Geometry g;
+  std::string err;
+  if (!g.init(dims, ndims, &err)) return fail(RBX_ERR_INVALID, err), -1;
+  const int es = dtype_size(dtype);
+  if (!es) return fail(RBX_ERR_INVALID, "unknown dtype"), -1;
+  int64_t total = 0;
+  for (int k = 0; k < nbufs; ++k)
+    if (counts[k]) total += rbx::inbox_buffer_bytes(g, (int64_t)counts[k], es);
+  return total;
+}
+
+int rbx_set_inbox(rbx_comm_t* c, void* ptr, size_t bytes, const rbx_ipc_handle_t* handles, const uint64_t* offsets) {
+  if (!c || c->nvirtual) return fail(RBX_ERR_INVALID, "not a per-rank communicator");
+  RBX_CUDA(cudaSetDevice(c->device));
+  RBX_CUDA(cudaDeviceSynchronize());  // no launch may still use the previous inbox
+  std::vector<char*> at(c->nranks, nullptr);
+  for (int q = 0; q < c->nranks; ++q) {
+    if (q == c->rank) {
+      at[q] = static_cast<char*>(ptr);
+      continue;
+    }
+    void* p = nullptr;
+    int rc = open_handle(handles[q], &p);
+    if (rc) return rc;
+    at[q] = static_cast<char*>(p) + offsets[q];
+  }
+  // cached MODE_PUSH plans point into the old inbox
+  for (auto it = c->plans.begin(); it != c->plans.end();) {
+    if (it->second.uses_inbox) {
+      cudaFree(it->second.dev);
+      cudaFree(it->second.ptrs);
+      it = c->plans.erase(it);
+    } else {
+      ++it;
+    }
+  }
+  c->inbox_local = static_cast<char*>(ptr);
+  c->inbox_bytes = bytes;
+  c->inbox_at = at;
   return RBX_OK;
 }
 
@@ -675,10 +776,37 @@ int rbx_vcollective_window(rbx_comm_t* c, void* const* bufs, size_t count, size_
   int nb = c->nblocks;
   if (local) nb = c->max_coresident > 0 ? c->max_coresident : c->sm_count;
   if (nb > RBX_MAX_BLOCKS) nb = RBX_MAX_BLOCKS;
+  const bool push = mode == RBX_MODE_PUSH && (op == RBX_OP_ALLREDUCE || op == RBX_OP_REDUCE_SCATTER);
+  if (push) {  // virtual ranks share this process: one local allocation holds every rank's inbox
+    const int64_t need = rbx::inbox_buffer_bytes(c->geo, (int64_t)count, es);
+    if ((int64_t)c->inbox_bytes < need) {
+      RBX_CUDA(cudaSetDevice(c->device));
+      RBX_CUDA(cudaDeviceSynchronize());
+      if (c->inbox_local) cudaFree(c->inbox_local);
+      c->inbox_local = nullptr;
+      c->inbox_bytes = 0;
+      for (auto pit = c->plans.begin(); pit != c->plans.end();) {
+        if (pit->second.uses_inbox) {
+          cudaFree(pit->second.dev);
+          cudaFree(pit->second.ptrs);
+          pit = c->plans.erase(pit);
+        } else {
+          ++pit;
+        }
+      }
+      RBX_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->inbox_local), (size_t)need * V));
+      c->inbox_owned = true;
+      c->inbox_bytes = (size_t)need;
+      c->inbox_at.assign(V, nullptr);
+      for (int r = 0; r < V; ++r) c->inbox_at[r] = c->inbox_local + (size_t)need * r;
+      it = c->plans.find(key);
+    }
+  }
   if (it == c->plans.end()) {
     std::string err;
     std::vector<void*> ptrs(bufs, bufs + V);
     std::vector<rbx::Plan> host(local ? 1 : V);
+    std::vector<std::vector<void*>> tables{ptrs};
     const int mis = misalign(ptrs, es);
     if (local) {
       if (!rbx::build_local_plan(c->geo, (int64_t)count, 16 / es, mis, nb, &host[0], &err, (int64_t)lo, (int64_t)hi))
@@ -692,14 +820,21 @@ int rbx_vcollective_window(rbx_comm_t* c, void* const* bufs, size_t count, size_
       spec.nblocks = nb;
       spec.lo = (int64_t)lo;
       spec.hi = (int64_t)hi;
+      if (push) tables.clear();
       for (int r = 0; r < V; ++r) {
         if (!rbx::build_plan(c->geo, r, (int64_t)count, spec, 0, &host[r], true, &err)) return fail(RBX_ERR_INVALID, err);
         for (int q = 0; q < V; ++q) host[r].sig[q] = c->sig[q];
         host[r].my_sig = c->sig[r];
+        if (push) {
+          std::vector<char*> cb;
+          for (void* p : ptrs) cb.push_back(static_cast<char*>(p));
+          tables.push_back(push_table(c->geo, r, (int64_t)count, es, mis, cb, c->inbox_at, 0));
+        }
       }
     }
     CachedPlan cp;
-    int rc = upload(c, host, ptrs, &cp);
+    cp.uses_inbox = push;
+    int rc = upload(c, host, tables, &cp);
     if (rc) return rc;
     it = c->plans.emplace(key, cp).first;
   }

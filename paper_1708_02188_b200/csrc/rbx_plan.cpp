@@ -327,7 +327,8 @@ bool build_plan(const Geometry& g, int me, int64_t count, const PlanSpec& spec, 
   std::vector<int> entry;
   int64_t o, l;
 
-  const Mode mode = spec.mode == MODE_AUTO ? MODE_FUSED : spec.mode;
+  Mode mode = spec.mode == MODE_AUTO ? MODE_FUSED : spec.mode;
+  if (mode == MODE_PUSH && spec.op == OP_ALLGATHER) mode = MODE_FUSED;  // allgather is push-only already
   if (spec.op == OP_BARRIER) {
     entry = peers;
     StepProto s0;
@@ -376,6 +377,34 @@ bool build_plan(const Geometry& g, int me, int64_t count, const PlanSpec& spec, 
       add_waits(exit.waits, (int)steps.size(), peers, false);
       steps.push_back(exit);
     }
+  } else if (mode == MODE_PUSH && spec.op != OP_ALLGATHER) {
+    // Two-shot, writes only.  Step 0: push my input of every peer's owned
+    // region into that peer's inbox (slot `me`).  Step 1: once every peer has
+    // pushed (ALL CTAs: the tile split of a region differs between the two
+    // steps), fold my region from my buffer and my inbox slots in the
+    // reference order and push the result into every buffer.  No peer ever
+    // reads my buffer, so no ENTRY wait is needed; the exit wait also
+    // guarantees peers are done reading their inboxes before my next call
+    // writes into them again.
+    const int R = n;
+    StepProto s0;
+    for (int q : rotated_after(peers, me)) {
+      int64_t qo, ql;
+      region(q, m, &qo, &ql);
+      segs.push_back(SegProto{0, qo, ql, {me}, single_level_ctrl(1), 1, {2 * R + q}});
+    }
+    s0.sigs = peers;
+    StepProto s1;
+    add_waits(s1.waits, 1, peers, true);
+    region(me, m, &o, &l);
+    std::vector<int> src;
+    for (int p : fold_order(g, me)) src.push_back(p == me ? me : R + p);
+    const bool ar = spec.op == OP_ALLREDUCE;
+    segs.push_back(SegProto{1, o, l, src, fold_ctrl(g), m, ar ? rotated_after(everyone, me) : std::vector<int>{me}});
+    s1.sigs = peers;
+    StepProto exit;
+    add_waits(exit.waits, 2, peers, false);
+    steps = {s0, s1, exit};
   } else if (mode == MODE_RING_DIMS) {
     std::vector<int> partners;
     for (int i = 0; i < m; ++i)
@@ -474,6 +503,18 @@ bool build_local_plan(const Geometry& g, int64_t count, int vec, int mis, int nb
     segs.push_back(SegProto{0, o, l, fold_order(g, r), ctrl, m, rotated_after(everyone, r)});
   }
   return add_segments(p, segs, 0, vec, mis, lo, hi < 0 ? count : hi, err);
+}
+
+int64_t inbox_slot_bytes(const Geometry& g, int64_t count, int itemsize) {
+  const int m = (int)g.active_dims().size();
+  int64_t maxlen = 0;
+  for (int r = 0; r < g.nranks; ++r) {
+    int64_t o, l;
+    region_after(g, r, count, m, &o, &l);
+    if (l > maxlen) maxlen = l;
+  }
+  const int64_t raw = maxlen * itemsize + 16;  // + phase pad (see rbx_capi.cu push_table)
+  return (raw + 255) / 256 * 256;
 }
 
 int64_t describe_plan(const Plan& p, int64_t* out, int64_t cap) {

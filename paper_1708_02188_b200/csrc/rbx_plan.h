@@ -33,7 +33,21 @@
 namespace rbx {
 
 enum Op : int32_t { OP_ALLREDUCE = 0, OP_REDUCE_SCATTER = 1, OP_ALLGATHER = 2, OP_BARRIER = 3 };
-enum Mode : int32_t { MODE_AUTO = 0, MODE_RING_DIMS = 1, MODE_FUSED = 2, MODE_FUSED_PULL = 3, MODE_LOCAL = 4 };
+enum Mode : int32_t {
+  MODE_AUTO = 0,
+  MODE_RING_DIMS = 1,
+  MODE_FUSED = 2,
+  MODE_FUSED_PULL = 3,
+  MODE_LOCAL = 4,
+  MODE_PUSH = 5  // two-shot, writes only: inputs pushed to the owners' inboxes, results pushed back
+};
+
+// Pointer-table layout per buffer in MODE_PUSH (entries relative to Seg.tbl):
+//   [0, R)    every rank's buffer
+//   [R, 2R)   this rank's inbox slot p (contribution of rank p to this rank's region)
+//   [2R, 3R)  rank q's inbox, this rank's slot (where this rank pushes q's region)
+// Other modes use only [0, R).
+inline int table_entries(int mode, int nranks) { return mode == MODE_PUSH ? 3 * nranks : nranks; }
 
 struct Seg {
   int64_t off, len;        // element range [off, off+len)
@@ -134,6 +148,13 @@ bool build_local_plan(const Geometry& g, int64_t count, int vec, int mis, int nb
                       int64_t lo = 0, int64_t hi = -1);
 // Flatten a plan into int64s for host-side inspection (tests).
 int64_t describe_plan(const Plan& p, int64_t* out, int64_t cap);
+
+// MODE_PUSH inbox geometry of one buffer: every owner keeps one slot per rank,
+// each large enough for the largest owned region plus a 16-byte phase pad.
+int64_t inbox_slot_bytes(const Geometry& g, int64_t count, int itemsize);
+inline int64_t inbox_buffer_bytes(const Geometry& g, int64_t count, int itemsize) {
+  return (int64_t)g.nranks * inbox_slot_bytes(g, count, itemsize);
+}
 
 }  // namespace rbx
 #endif

@@ -186,6 +186,8 @@ class RankContext:
         arr = (_native.IpcHandle * grid.size)(*[_native.IpcHandle.from_raw(x) for x in handles])
         _native.check(self._L.rbx_comm_connect(self._comm, arr))
         self._registered: dict = {}  # data_ptr -> (nbytes, tensor kept alive)
+        self._inbox = None
+        self._inbox_bytes = 0
         self._agreed: set = set()
         self._staging: dict = {}
         self._traffic: dict = {}
@@ -266,6 +268,30 @@ class RankContext:
         _native.check(self._L.rbx_register_buffer(self._comm, ctypes.c_void_p(ptr), nbytes, hs, offs, ctypes.byref(bid)))
         self._registered[ptr] = (nbytes, tensor)
 
+    def _ensure_inbox(self, counts, dtype: str, op: str, mode: int) -> None:
+        """MODE_PUSH needs a symmetric inbox (~1x the buffer bytes); grow it
+        collectively when a larger buffer shows up (all ranks make the same
+        calls with the same counts, so they grow together)."""
+        if mode != _native.MODES["push"] or op not in ("allreduce", "reduce_scatter", "buckets", "window"):
+            return
+        need = _native.inbox_bytes(list(self.grid.dims), list(counts), dtype)
+        if need <= self._inbox_bytes:
+            return
+        torch = _torch()
+        nbytes = max(need, 2 * self._inbox_bytes)
+        inbox = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        h = _native.IpcHandle()
+        off = ctypes.c_uint64()
+        _native.check(self._L.rbx_export_buffer(ctypes.c_void_p(inbox.data_ptr()), ctypes.byref(h), ctypes.byref(off)))
+        items = allgather_objects((h.to_bytes(), off.value, nbytes), self.group)
+        if len({x[2] for x in items}) != 1:
+            raise CollectiveError("inbox size mismatch across ranks", rank=None)
+        hs = (_native.IpcHandle * len(items))(*[_native.IpcHandle.from_raw(x[0]) for x in items])
+        offs = (ctypes.c_uint64 * len(items))(*[x[1] for x in items])
+        _native.check(self._L.rbx_set_inbox(self._comm, ctypes.c_void_p(inbox.data_ptr()), nbytes, hs, offs))
+        self._inbox = inbox
+        self._inbox_bytes = nbytes
+
     def _ensure(self, tensor) -> None:
         if tensor.numel() == 0:
             return
@@ -310,6 +336,7 @@ class RankContext:
             return (0, 0)
         self._ensure(tensor)
         self._agree_shape((tensor.data_ptr(), op, n, dt, m))
+        self._ensure_inbox([n], dt, op, m)
         code = _native.DTYPE_CODES[dt]
         ptr = ctypes.c_void_p(tensor.data_ptr())
         owned = (0, n)
@@ -339,6 +366,7 @@ class RankContext:
             raise ValueError(f"window [{lo}, {hi}) outside [0, {n}]")
         self._ensure(tensor)
         self._agree_shape((tensor.data_ptr(), "window", n, lo, hi, dt, m))
+        self._ensure_inbox([n], dt, "window", m)
         _native.check(self._L.rbx_allreduce_window(self._comm, ctypes.c_void_p(tensor.data_ptr()), n, lo, hi,
                                                    _native.DTYPE_CODES[dt], m, self.stream()))
         if self.blocking:
@@ -356,6 +384,7 @@ class RankContext:
             self._ensure(t)
         m = _native.MODES[mode or self.mode]
         self._agree_shape((tuple(t.data_ptr() for t in tensors), "buckets", tuple(t.numel() for t in tensors), dt, m))
+        self._ensure_inbox([t.numel() for t in tensors], dt, "buckets", m)
         ptrs = (ctypes.c_void_p * len(tensors))(*[t.data_ptr() for t in tensors])
         counts = (ctypes.c_size_t * len(tensors))(*[t.numel() for t in tensors])
         _native.check(self._L.rbx_allreduce_buckets(self._comm, ptrs, counts, len(tensors), _native.DTYPE_CODES[dt], m,

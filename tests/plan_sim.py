@@ -33,6 +33,17 @@ def simulate(dims, bufs, op="allreduce", mode="fused", nb=3, seed=0, dtype="f32"
     count = len(bufs[0])
     plans = [_native.parse_plan(_native.plan_describe(dims, r, count, op, mode, dtype)) for r in range(n)]
     bufs = [b.copy() for b in bufs]
+    inbox = {}  # MODE_PUSH: (owner, slot) -> element-offset-addressed array
+
+    def resolve(me, idx):
+        """Pointer-table entry -> array (rbx_plan.h table_entries layout)."""
+        if idx < n:
+            return bufs[idx]
+        key = (me, idx - n) if idx < 2 * n else (idx - 2 * n, me)
+        if key not in inbox:
+            inbox[key] = np.full(count, np.nan if bufs[0].dtype.kind == "f" else -7, dtype=bufs[0].dtype)
+        return inbox[key]
+
     flags = {}  # (dst_rank, slot, src_rank, block) -> 1
     pos = {(r, b): -1 for r in range(n) for b in range(nb)}  # -1: entry not yet signalled
     rng = random.Random(seed)
@@ -74,10 +85,10 @@ def simulate(dims, bufs, op="allreduce", mode="fused", nb=3, seed=0, dtype="f32"
                 a, z = max(lo, base), min(hi, base + sg["len"])
                 if a < z:
                     o0, o1 = sg["off"] + a - base, sg["off"] + z - base
-                    vals = [bufs[q][o0:o1] for q in sg["src"]]
+                    vals = [resolve(r, q)[o0:o1] for q in sg["src"]]
                     res = vals[0].copy() if len(vals) == 1 else _fold(vals, sg["ctrl"], sg["nlev"])
                     for q in sg["dst"]:
-                        bufs[q][o0:o1] = res
+                        resolve(r, q)[o0:o1] = res
                 base += sg["len"]
             for q in st["sigs"]:
                 flags[(q, s + 1, r, b)] = 1

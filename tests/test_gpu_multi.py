@@ -101,7 +101,7 @@ def test_all_decompositions_all_modes_bit_exact(world):
     lengths = [0, 1, 17, 1000, 4099]
     cases = []
     for dims in _dims_for(world):
-        for mode in ("fused", "fused_pull", "ring_dims"):
+        for mode in ("fused", "fused_pull", "ring_dims", "push"):
             for dtype in ("f32", "i64", "f64"):
                 cases.append({"dims": dims, "mode": mode, "dtype": dtype, "lengths": lengths, "seed": world})
     res = _spawn(world, cases)
@@ -134,7 +134,7 @@ def test_reduce_scatter_allgather_pair(world):
     if cuda_count() < world:
         pytest.skip(f"needs {world} GPUs")
     cases = [{"dims": d, "mode": m, "dtype": "f32", "lengths": [10007, 1], "seed": 11, "op": "rs+ag"}
-             for d in _dims_for(world) for m in ("fused", "ring_dims")]
+             for d in _dims_for(world) for m in ("fused", "ring_dims", "push")]
     res = _spawn(world, cases)
     for r in range(world):
         for dims, mode, dtype, it, length, op, dig, _ in res[r][2]:
@@ -149,7 +149,7 @@ def test_full_size_config(world):
         pytest.skip(f"needs {world} GPUs")
     n = 25_600_000
     cases = [{"dims": d, "mode": m, "dtype": "f32", "lengths": [n], "seed": 0}
-             for d in ([(2, 4), (2, 2, 2)] if world == 8 else _dims_for(world)[:1]) for m in ("fused", "ring_dims")]
+             for d in ([(2, 4), (2, 2, 2)] if world == 8 else _dims_for(world)[:1]) for m in ("fused", "ring_dims", "push")]
     res = _spawn(world, cases)
     large = golden("large_digests")
     for r in range(world):

@@ -50,7 +50,7 @@ def run(vr, parts, op, mode, dtype_t):
     return [t.cpu().numpy() for t in ts]
 
 
-@pytest.mark.parametrize("mode", ["local", "fused", "fused_pull", "ring_dims"])
+@pytest.mark.parametrize("mode", ["local", "fused", "fused_pull", "ring_dims", "push"])
 def test_all_decompositions_bit_exact(mode):
     """tests/golden/replay_digests.json: reference acceptance sweep
     (pkg/tests/test_acceptance.py:41-73) on the GPU, f32/f64/i64."""
@@ -73,7 +73,7 @@ def test_all_decompositions_bit_exact(mode):
 
 @pytest.mark.parametrize("dims", [(2, 4), (2, 2, 2), (8,), (4, 2)])
 @pytest.mark.parametrize("length", [25_600_000, 25_557_032])
-@pytest.mark.parametrize("mode", ["local", "fused", "ring_dims"])
+@pytest.mark.parametrize("mode", ["local", "fused", "ring_dims", "push"])
 def test_full_size_configs(dims, length, mode):
     """Configs 1/2 at full size (102.4 MB fp32 per rank) vs the reference digest."""
     torch = _torch()
@@ -88,7 +88,7 @@ def test_full_size_configs(dims, length, mode):
     del torch
 
 
-@pytest.mark.parametrize("mode", ["fused", "ring_dims"])
+@pytest.mark.parametrize("mode", ["fused", "ring_dims", "push"])
 def test_reduce_scatter_then_allgather(mode):
     torch = _torch()
     from paper_1708_02188_b200.virtual import VirtualRanks
@@ -117,7 +117,7 @@ def test_reduce_scatter_then_allgather(mode):
         vr.close()
 
 
-@pytest.mark.parametrize("mode", ["local", "fused", "ring_dims"])
+@pytest.mark.parametrize("mode", ["local", "fused", "ring_dims", "push"])
 def test_bf16_f16_fp32_accumulate(mode):
     """bf16/f16: fold fp32-upcast inputs in the reference order, one RNE at the
     end (parity unpinned by the reference, which has no bf16: runtime.py:37)."""
@@ -169,7 +169,7 @@ def test_repeated_calls_epochs_and_launch_count():
         length = int(rng.integers(1, 50_000))
         parts = [rng.integers(-1000, 1001, length).astype(np.int64) for _ in range(8)]
         ts = [torch.from_numpy(p).cuda() for p in parts]
-        mode = ["fused", "ring_dims", "fused_pull"][k % 3]
+        mode = ["fused", "ring_dims", "fused_pull", "push"][k % 4]
         vr.collective(ts, mode=mode)
         torch.cuda.synchronize()
         vr.check()
@@ -180,7 +180,7 @@ def test_repeated_calls_epochs_and_launch_count():
     vr.close()
 
 
-@pytest.mark.parametrize("mode", ["local", "fused"])
+@pytest.mark.parametrize("mode", ["local", "fused", "push"])
 def test_cuda_graph_replay(mode):
     """Epochs live in device memory, so a captured launch replays correctly
     (CUDA graphs instead of per-call launches for static buffers)."""
@@ -215,7 +215,7 @@ def test_cuda_graph_replay(mode):
     vr.close()
 
 
-@pytest.mark.parametrize("mode", ["local", "fused", "ring_dims"])
+@pytest.mark.parametrize("mode", ["local", "fused", "ring_dims", "push"])
 def test_windows_compose_to_the_full_allreduce(mode):
     """rbx_vcollective_window: element windows keep the full buffer's chunk
     geometry and order, so any split reproduces the full result bit-for-bit."""

@@ -73,7 +73,7 @@ def test_plan_rejects_bad_geometry():
         _native.plan_describe((0,), 0, 10)
 
 
-@pytest.mark.parametrize("mode", ["fused", "fused_pull", "ring_dims"])
+@pytest.mark.parametrize("mode", ["fused", "fused_pull", "ring_dims", "push"])
 def test_plan_tables_reproduce_reference_allreduce(mode):
     """Simulate every rank's step table (3 CTAs/rank, random interleavings) and
     compare with the reference replay digests for all decompositions."""
@@ -89,7 +89,7 @@ def test_plan_tables_reproduce_reference_allreduce(mode):
             assert {orc.sha256(b) for b in out} == {want}, (mode, dims, length)
 
 
-@pytest.mark.parametrize("mode", ["fused", "ring_dims"])
+@pytest.mark.parametrize("mode", ["fused", "ring_dims", "push"])
 def test_plan_tables_reduce_scatter_and_allgather(mode):
     for n, dims in [(2, (2,)), (4, (2, 2)), (6, (3, 2)), (8, (2, 2, 2)), (8, (2, 4)), (8, (8,))]:
         grid = orc.Grid(dims)
