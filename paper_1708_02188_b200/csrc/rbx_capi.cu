@@ -23,7 +23,15 @@
 #include "rbx_kernel.cuh"
 #include "rbx_plan.h"
 
+#include "rbx_local.cuh"
+
 namespace rbx {
+const void* local_kernel_f32(int v, int nlev);
+const void* local_kernel_f64(int v, int nlev);
+const void* local_kernel_i64(int v, int nlev);
+const void* local_kernel_bf16(int v, int nlev);
+const void* local_kernel_f16(int v, int nlev);
+const void* local_kernel_i32(int v, int nlev);
 const void* step_kernel_f32();
 const void* step_kernel_f64();
 const void* step_kernel_i64();
@@ -74,6 +82,9 @@ struct CachedPlan {
   int nplans = 0;
   int plan_bytes = 0;  // staged into shared memory by every CTA
   bool uses_inbox = false;
+  const void* local_fn = nullptr;  // specialised MODE_LOCAL kernel (rbx_local.cuh), if the shape has one
+  std::shared_ptr<rbx::LocalArgs> local_args;
+  int local_grid = 0;
 };
 
 struct OpenedHandle {
@@ -104,6 +115,7 @@ struct rbx_comm {
   size_t bytes_per_cta = 32 * 1024;   // adaptive CTA count per call; env RBX_BYTES_PER_CTA
   int min_blocks = 16;                // env RBX_MIN_BLOCKS
   unsigned long long* trace_dev = nullptr;  // 64-word kernel timeline when RBX_TRACE is set
+  bool local_specialised = true;  // MODE_LOCAL uses rbx_local_kernel where the shape has one; env RBX_LOCAL_GENERIC=1
   // MODE_PUSH inboxes: this rank's (registered, symmetric) and every rank's mapping
   char* inbox_local = nullptr;
   size_t inbox_bytes = 0;
@@ -148,6 +160,48 @@ const void* kernel_for(int dtype) {
   }
 }
 
+const void* local_kernel_for(int dtype, int v, int nlev) {
+  switch (dtype) {
+    case RBX_F32: return rbx::local_kernel_f32(v, nlev);
+    case RBX_F64: return rbx::local_kernel_f64(v, nlev);
+    case RBX_I64: return rbx::local_kernel_i64(v, nlev);
+    case RBX_BF16: return rbx::local_kernel_bf16(v, nlev);
+    case RBX_F16: return rbx::local_kernel_f16(v, nlev);
+    case RBX_I32: return rbx::local_kernel_i32(v, nlev);
+    default: return nullptr;
+  }
+}
+
+// Kernel arguments of the specialised local kernel from a MODE_LOCAL plan
+// (one step, one segment per owned region, all V buffers as destinations).
+bool local_args_from_plan(const rbx::Plan& p, const std::vector<void*>& bufs, rbx::LocalArgs* a) {
+  std::memset(a, 0, sizeof(*a));
+  if (p.nsteps != 1) return false;
+  const rbx::Step& st = p.steps[0];
+  if (st.nseg > RBX_LOCAL_MAX_SEGS) return false;
+  a->nseg = st.nseg;
+  a->total_vec = st.total_vec;
+  for (size_t d = 0; d < bufs.size(); ++d) a->dst[d] = static_cast<char*>(bufs[d]);
+  for (int k = 0; k < st.nseg; ++k) {
+    const rbx::Seg& sg = p.segs[st.seg0 + k];
+    rbx::LocalSeg& ls = a->seg[k];
+    ls.vec_begin = sg.vec_begin;
+    ls.nvec = sg.nvec;
+    ls.body_off = sg.body_off;
+    for (int j = 0; j < sg.nsrc; ++j) {
+      ls.src[j] = static_cast<const char*>(bufs[sg.src[j]]);
+      ls.ctrl[j] = sg.ctrl[j];
+    }
+    for (int i = 0; i < sg.head + sg.tail; ++i) {
+      if (a->nscalar >= (int)(sizeof(a->scalar_elem) / sizeof(a->scalar_elem[0]))) return false;
+      a->scalar_elem[a->nscalar] = i < sg.head ? sg.off + i : sg.body_off + sg.nvec * p.vec + (i - sg.head);
+      a->scalar_seg[a->nscalar] = (uint8_t)k;
+      a->nscalar++;
+    }
+  }
+  return true;
+}
+
 int coresident_blocks(int device, int threads, int* out) {
   int sms = 0;
   RBX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
@@ -173,6 +227,7 @@ int common_init(rbx_comm* c, const int* dims, int ndims, int device, int threads
   c->device = device;
   if (const char* t = std::getenv("RBX_TILE")) c->tile = std::atoi(t);
   if (const char* t = std::getenv("RBX_LOCAL_TILE")) c->local_tile = std::atoi(t);
+  if (const char* t = std::getenv("RBX_LOCAL_GENERIC")) c->local_specialised = std::atoi(t) == 0;
   if (const char* t = std::getenv("RBX_BYTES_PER_CTA")) c->bytes_per_cta = (size_t)std::max(1L, std::atol(t));
   if (const char* t = std::getenv("RBX_MIN_BLOCKS")) c->min_blocks = std::max(1, std::atoi(t));
   RBX_CUDA(cudaSetDevice(device));
@@ -836,7 +891,25 @@ int rbx_vcollective_window(rbx_comm_t* c, void* const* bufs, size_t count, size_
     cp.uses_inbox = push;
     int rc = upload(c, host, tables, &cp);
     if (rc) return rc;
+    if (local && c->local_specialised) {
+      const void* fn = local_kernel_for(dtype, V, (int)c->geo.active_dims().size());
+      auto args = std::make_shared<rbx::LocalArgs>();
+      if (fn && local_args_from_plan(host[0], ptrs, args.get())) {
+        int per_sm = 0;
+        RBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, c->threads, 0));
+        cp.local_fn = fn;
+        cp.local_args = args;
+        cp.local_grid = std::max(1, per_sm) * c->sm_count;
+      }
+    }
     it = c->plans.emplace(key, cp).first;
+  }
+  if (it->second.local_fn) {  // specialised local-reduce kernel (no step table, no flags)
+    void* params[] = {it->second.local_args.get()};
+    RBX_CUDA(cudaLaunchKernel(it->second.local_fn, dim3((unsigned)it->second.local_grid), dim3((unsigned)c->threads),
+                              params, 0, (cudaStream_t)stream));
+    c->launches++;
+    return RBX_OK;
   }
   if (!local && (int64_t)nb * V > c->max_coresident)
     return fail(RBX_ERR_INVALID, "virtual ranks x blocks exceed co-resident CTAs");

@@ -1,6 +1,16 @@
-// Instantiation of the step kernel for dtype f64 (one TU per dtype: parallel builds).
+// Instantiations for dtype f64 (one TU per dtype: parallel builds): the step
+// kernel and the specialised local-reduce kernels.
 #include "rbx_kernel.cuh"
+#include "rbx_local.cuh"
 
 namespace rbx {
 const void* step_kernel_f64() { return reinterpret_cast<const void*>(&rbx_step_kernel<double>); }
+
+const void* local_kernel_f64(int v, int nlev) {
+#define RBX_LOCAL_CASE(V, L) \
+  if (v == V && nlev == L) return reinterpret_cast<const void*>(&rbx_local_kernel<double, V, L>);
+  RBX_LOCAL_SHAPES(RBX_LOCAL_CASE)
+#undef RBX_LOCAL_CASE
+  return nullptr;
+}
 }  // namespace rbx
