@@ -219,6 +219,63 @@ def test_bucket_list_one_launch(world):
             assert digs[k] == orc.sha256(orc.closed_form_allreduce(orc.Grid(dims), parts))
 
 
+def _calib_main(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1708_02188_b200.calibrate import calibrated_topology
+    from paper_1708_02188_b200.multiring import Grid, plan
+    from paper_1708_02188_b200.runtime import RankContext
+
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ctx = RankContext(rank, Grid((world,)), device=rank, blocking=False)
+        t, m = calibrated_topology(ctx, big_elems=16 * 1024 * 1024, iters=4)
+        p = plan(t, t.devices(), 0.1024)
+        # errors surface as the reference's exception types
+        errs = []
+        stray = torch.empty(1000, device=f"cuda:{rank}")
+        try:
+            import ctypes
+
+            from paper_1708_02188_b200 import _native
+
+            _native.check(ctx._L.rbx_allreduce(ctx._comm, ctypes.c_void_p(stray.data_ptr()), 1000, 0, 0, None))
+        except ValueError as exc:
+            errs.append("unregistered:" + str(exc)[:40])
+        q.put((rank, "ok", m, p.grid.dims, errs))
+        ctx.close()
+    except Exception as exc:  # noqa: BLE001
+        q.put((rank, "error", repr(exc), None, None))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_planner_calibration_and_abi_errors():
+    """measured per-stage latency and bus bandwidth feed the
+    reference planner through a B200 topology; unregistered buffers are refused."""
+    if cuda_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_calib_main, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    for rank, status, m, dims, errs in res:
+        assert status == "ok", m
+        assert 0 < m["latency_s"] < 1e-3 and m["bandwidth_gbps"] > 100
+        assert dims == (2,)
+        assert errs and errs[0].startswith("unregistered:buffer is not registered")
+
+
 def test_launch_api_matches_reference_and_detects_faults():
     """`launch` (runtime.py:435-589): serial-oracle digests for i64, a crashed
     rank is attributed, a shape mismatch aborts."""
