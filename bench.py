@@ -16,9 +16,11 @@ own generator (`generate_input`, seed 0).
 Metric definitions (NCCL convention): algbw = S/t,
 busbw = 2(R-1)/R * S / t for R ranks.  `value` = busbw summed over the
 physical GPUs (N * busbw; at N = 1 the single GPU's busbw).  Every step
-restores the inputs and flushes L2 (256 MiB write) outside the timed region;
-the timed region is one allreduce, CUDA events on the launching stream,
-max over ranks.
+restores the inputs and flushes L2 (256 MiB write, read back so no dirty
+lines are charged to the kernel) outside the timed region; the timed region
+is one allreduce, CUDA events on the launching stream, max over ranks.
+`--impl reference` runs the reference runtime's phase loop ported to C
+(oracle/rbx_oracle.c, one thread per rank) on the host on the same job.
 """
 
 from __future__ import annotations
@@ -179,6 +181,11 @@ def flush_l2(scratch):
     torch.cuda._sleep(100_000)
 
 
+def workload_name(n: int, dtype: str, ranks: int, dims) -> str:
+    """Same string on every arm (ours / --impl reference) for the same job."""
+    return f"config2: {n} {dtype}/rank, {ranks} ranks, grid {'x'.join(map(str, dims))}"
+
+
 def busbw(ranks: int, nbytes: int, seconds: float) -> float:
     return 2.0 * (ranks - 1) / ranks * nbytes / seconds / 1e9
 
@@ -228,7 +235,7 @@ def run_reference(args):
         "impl": "reference", "value": round(value, 4), "unit": "GB/s", "n_gpus": n_gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference generate_input, seed 0)",
-        "config": {"workload": f"config2: {args.elems} fp32/rank, {ranks} ranks, grid {'x'.join(map(str, dims))}",
+        "config": {"workload": workload_name(args.elems, "f32", ranks, dims), "placement": f"CPU, {ranks} threads",
                    "ranks": ranks, "dims": list(dims), "bytes_per_rank": nbytes},
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": min(ranks, cores), "kind": "port",
                          "sample": f"{args.steps} full allreduces of {args.elems} fp32 x {ranks} ranks "
@@ -324,7 +331,7 @@ def main_single(args):
     peak, peak_src = hbm_peak()
     hbm_bytes = 2 * ranks * nbytes  # read every rank buffer once, write every rank buffer once
     achieved = hbm_bytes / t / 1e9
-    workload = f"config2-local: {n} {args.dtype}/rank x {ranks} virtual ranks, grid {'x'.join(map(str, dims))}, 1 GPU"
+    workload = workload_name(n, args.dtype, ranks, dims)
     traffic = ncu_traffic("local_2x2x2_25.6M_f32") if (dims == (2, 2, 2) and n == N_ELEM and args.dtype == "f32") else None
 
     cpu = None
@@ -342,7 +349,8 @@ def main_single(args):
         "value": round(bw, 3), "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(t * 1e3, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": args.dtype, "data": "synthetic (reference generate_input, seed 0)",
-        "config": {"workload": workload, "ranks": ranks, "dims": list(dims), "bytes_per_rank": nbytes,
+        "config": {"workload": workload, "placement": "1 GPU: all ranks' buffers in HBM, local-reduce kernel",
+                   "ranks": ranks, "dims": list(dims), "bytes_per_rank": nbytes,
                    "mode": "local", "l2": "flushed between steps (256 MiB write) and inputs 819 MB > L2",
                    "value_definition": "busbw = 2(R-1)/R*S/t per (virtual) rank; 1 GPU"},
         "busbw_gbs": round(bw, 3), "algbw_gbs": round(nbytes / t / 1e9, 3),
@@ -472,7 +480,7 @@ def main_multi(args):
             "value": round(bw * world, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t * 1e3, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (reference generate_input, seed 0)",
-            "config": {"workload": f"config2: {n} {args.dtype}/rank, grid {'x'.join(map(str, dims))}, {world} GPUs",
+            "config": {"workload": workload_name(n, args.dtype, world, dims), "placement": f"{world} GPUs, one rank each",
                        "ranks": world, "dims": list(dims), "bytes_per_rank": nbytes, "mode": args.mode,
                        "l2": "flushed between steps (256 MiB write per rank)",
                        "value_definition": "N * busbw, busbw = 2(N-1)/N*S/t (NCCL convention), max over ranks"},
