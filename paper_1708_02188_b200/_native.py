@@ -183,7 +183,7 @@ def parse_plan(words: list) -> dict:
             sg["ctrl"] = [nxt() for _ in range(ns)]
             sg["nlev"] = nxt()
             sg["dst"] = [nxt() for _ in range(nxt())]
-            sg["tbl"], sg["head"], sg["nvec"], sg["tail"] = nxt(), nxt(), nxt(), nxt()
+            sg["tbl"], sg["head"], sg["nvec"], sg["tail"], sg["acc"] = nxt(), nxt(), nxt(), nxt(), nxt()
             st["segs"].append(sg)
         plan["steps"].append(st)
     return plan

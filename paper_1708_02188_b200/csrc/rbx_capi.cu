@@ -311,9 +311,7 @@ int launch(rbx_comm* c, const CachedPlan& cp, int dtype, cudaStream_t stream, bo
 // fp32-partial workspace for that is not built yet, so refuse rather than
 // silently round partials (parity policy: one RNE at the end).
 int check_mode_dtype(int mode, int dtype) {
-  if (mode == RBX_MODE_RING_DIMS && (dtype == RBX_BF16 || dtype == RBX_F16))
-    return fail(RBX_ERR_UNSUPPORTED, "MODE_RING_DIMS with bf16/f16 needs fp32 partial workspaces (not implemented); "
-                                     "use MODE_FUSED, which folds in fp32 and rounds once");
+  (void)dtype;
   if (mode < RBX_MODE_AUTO || mode > RBX_MODE_PUSH) return fail(RBX_ERR_INVALID, "unknown mode");
   return RBX_OK;
 }
@@ -341,6 +339,29 @@ std::vector<void*> push_table(const rbx::Geometry& g, int me, int64_t count, int
   for (int p = 0; p < R; ++p) t[R + p] = biased(me, p);
   for (int q = 0; q < R; ++q) t[2 * R + q] = biased(q, me);
   return t;
+}
+
+// RING_DIMS bf16/f16 pointer table: buffers, then every rank's fp32 partial
+// workspace (carved from its inbox), biased so the plan's element offsets
+// address it and element vectors stay 32-byte aligned like in the buffer.
+std::vector<void*> ws_table(const rbx::Geometry& g, int64_t count, int es, int mis, const std::vector<char*>& bufs,
+                            const std::vector<char*>& inbox, int64_t inbox_off) {
+  const int R = g.nranks;
+  const int vec = 16 / es;
+  std::vector<void*> t(2 * R, nullptr);
+  for (int q = 0; q < R; ++q) {
+    t[q] = bufs[q];
+    int64_t o, l;
+    rbx::region_after(g, q, count, 1, &o, &l);  // region after the first ring dimension
+    const int64_t pad = mis >= 0 ? (mis + o) % vec : 0;
+    t[R + q] = reinterpret_cast<void*>(reinterpret_cast<uintptr_t>(inbox[q]) + inbox_off + (pad - o) * 4);
+  }
+  return t;
+}
+
+bool needs_fp32_partials(const rbx::Geometry& g, int mode, int dtype, int op) {
+  return mode == RBX_MODE_RING_DIMS && (dtype == RBX_BF16 || dtype == RBX_F16) && g.active_dims().size() > 1 &&
+         (op == RBX_OP_ALLREDUCE || op == RBX_OP_REDUCE_SCATTER);
 }
 
 // Elements between the previous 16-byte boundary and element 0, if identical
@@ -399,7 +420,10 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
     spec.lo = lo;
     spec.hi = hi;
     const bool push = mode == RBX_MODE_PUSH && (op == RBX_OP_ALLREDUCE || op == RBX_OP_REDUCE_SCATTER);
-    const int E = push ? 3 * c->nranks : c->nranks;  // pointer-table entries per buffer
+    const bool ws = needs_fp32_partials(c->geo, mode, dtype, op);
+    spec.partials_fp32 = ws;
+    // pointer-table entries per buffer
+    const int E = push ? 3 * c->nranks : (ws ? 2 * c->nranks : c->nranks);
     int64_t inbox_off = 0;
     std::string err;
     for (int k = 0; k < nbufs; ++k) {
@@ -413,14 +437,15 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
         std::vector<char*> mine;
         for (int q = 0; q < c->nranks; ++q) mine.push_back(c->bufs[id].at[q] + off);
         spec.mis = misalign(std::vector<void*>(mine.begin(), mine.end()), es);
-        if (push) {
+        if (push || ws) {
           const int64_t need = rbx::inbox_buffer_bytes(c->geo, (int64_t)counts[k], es);
           if (inbox_off + need > (int64_t)c->inbox_bytes)
-            return fail(RBX_ERR_INVALID, "MODE_PUSH inbox too small: need " + std::to_string(inbox_off + need) +
+            return fail(RBX_ERR_INVALID, "inbox too small for this mode: need " + std::to_string(inbox_off + need) +
                                              " bytes, have " + std::to_string(c->inbox_bytes) +
                                              " (rbx_set_inbox; size with rbx_inbox_bytes)");
-          std::vector<void*> t = push_table(c->geo, c->rank, (int64_t)counts[k], es, spec.mis, mine, c->inbox_at,
-                                            inbox_off);
+          std::vector<void*> t = push ? push_table(c->geo, c->rank, (int64_t)counts[k], es, spec.mis, mine,
+                                                   c->inbox_at, inbox_off)
+                                      : ws_table(c->geo, (int64_t)counts[k], es, spec.mis, mine, c->inbox_at, inbox_off);
           ptrs.insert(ptrs.end(), t.begin(), t.end());
           inbox_off += need;
         } else {
@@ -433,7 +458,7 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
     for (int q = 0; q < c->nranks; ++q) host[0].sig[q] = c->sig[q];
     host[0].my_sig = c->sig[c->rank];
     CachedPlan cp;
-    cp.uses_inbox = push;
+    cp.uses_inbox = push || ws;
     int rc = upload(c, host, {ptrs}, &cp);
     if (rc) return rc;
     it = c->plans.emplace(key, cp).first;
@@ -832,7 +857,8 @@ int rbx_vcollective_window(rbx_comm_t* c, void* const* bufs, size_t count, size_
   if (local) nb = c->max_coresident > 0 ? c->max_coresident : c->sm_count;
   if (nb > RBX_MAX_BLOCKS) nb = RBX_MAX_BLOCKS;
   const bool push = mode == RBX_MODE_PUSH && (op == RBX_OP_ALLREDUCE || op == RBX_OP_REDUCE_SCATTER);
-  if (push) {  // virtual ranks share this process: one local allocation holds every rank's inbox
+  const bool ws = needs_fp32_partials(c->geo, mode, dtype, op);
+  if (push || ws) {  // virtual ranks share this process: one local allocation holds every rank's inbox
     const int64_t need = rbx::inbox_buffer_bytes(c->geo, (int64_t)count, es);
     if ((int64_t)c->inbox_bytes < need) {
       RBX_CUDA(cudaSetDevice(c->device));
@@ -875,7 +901,13 @@ int rbx_vcollective_window(rbx_comm_t* c, void* const* bufs, size_t count, size_
       spec.nblocks = nb;
       spec.lo = (int64_t)lo;
       spec.hi = (int64_t)hi;
+      spec.partials_fp32 = ws;
       if (push) tables.clear();
+      if (ws) {
+        std::vector<char*> cb;
+        for (void* p : ptrs) cb.push_back(static_cast<char*>(p));
+        tables = {ws_table(c->geo, (int64_t)count, es, mis, cb, c->inbox_at, 0)};
+      }
       for (int r = 0; r < V; ++r) {
         if (!rbx::build_plan(c->geo, r, (int64_t)count, spec, 0, &host[r], true, &err)) return fail(RBX_ERR_INVALID, err);
         for (int q = 0; q < V; ++q) host[r].sig[q] = c->sig[q];
@@ -888,7 +920,7 @@ int rbx_vcollective_window(rbx_comm_t* c, void* const* bufs, size_t count, size_
       }
     }
     CachedPlan cp;
-    cp.uses_inbox = push;
+    cp.uses_inbox = push || ws;
     int rc = upload(c, host, tables, &cp);
     if (rc) return rc;
     if (local && c->local_specialised) {

@@ -300,6 +300,125 @@ __device__ __forceinline__ void fold_scalar(const SegCtx& sc, int64_t elem) {
   for (int d = 0; d < sc.ndst; ++d) __stcg(reinterpret_cast<B*>(sc.dst[d] + byte), out);
 }
 
+// ---- RING_DIMS with bf16/f16: stage partials kept in fp32 workspaces --------
+// One ring fold (single level) where the sources (ACC bit0) and/or the
+// destinations (ACC bit1) are fp32 partial arrays instead of T buffers: a
+// vector unit is VEC elements (16 bytes of T, 32 bytes of fp32).  Rounding to
+// T happens once, in the last dimension's fold (parity policy: fold the
+// fp32-upcast inputs in the reference order, one RNE at the end).
+template <typename T, int NSRC, int ACC>
+__device__ __noinline__ void fold_body_acc(const SegCtx& sc, int64_t body_off, int64_t v0, int64_t v1) {
+  using Acc = typename Traits<T>::Acc;
+  constexpr int VEC = Traits<T>::VEC;
+  if constexpr (sizeof(Acc) == 4 && VEC == 8) {
+    for (int64_t v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+      const int64_t e = body_off + v * VEC;  // first element of this vector
+      constexpr int B = NSRC < 4 ? NSRC : 4;  // operands per load batch (8 x 16-byte loads in flight)
+      FoldState<T, VEC, 1> st;
+#pragma unroll
+      for (int j0 = 0; j0 < NSRC; j0 += B) {
+        int4 raw[B][2];
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+          if (j0 + k < NSRC) {
+            if (ACC & 1) {
+              raw[k][0] = ld_stream(sc.src[j0 + k] + e * 4);
+              raw[k][1] = ld_stream(sc.src[j0 + k] + e * 4 + 16);
+            } else {
+              raw[k][0] = ld_stream(sc.src[j0 + k] + e * (int64_t)sizeof(T));
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+          if (j0 + k < NSRC) {
+            Acc x[VEC];
+#pragma unroll
+            for (int l = 0; l < VEC; ++l)
+              x[l] = (ACC & 1) ? __uint_as_float(word(raw[k][l >> 2], l & 3)) : Traits<T>::lane(raw[k][0], l);
+            st.feed(sc.ctrl[j0 + k], x);
+          }
+        }
+      }
+      if (ACC & 2) {
+        int4 lo, hi;
+        lo = make_int4(__float_as_int(st.result(0)), __float_as_int(st.result(1)), __float_as_int(st.result(2)),
+                       __float_as_int(st.result(3)));
+        hi = make_int4(__float_as_int(st.result(4)), __float_as_int(st.result(5)), __float_as_int(st.result(6)),
+                       __float_as_int(st.result(7)));
+        for (int d = 0; d < sc.ndst; ++d) {
+          __stcg(reinterpret_cast<int4*>(sc.dst[d] + e * 4), lo);
+          __stcg(reinterpret_cast<int4*>(sc.dst[d] + e * 4 + 16), hi);
+        }
+      } else {
+        int4 packed = make_int4(0, 0, 0, 0);
+#pragma unroll
+        for (int l = 0; l < VEC; ++l) Traits<T>::put(packed, l, st.result(l));
+        for (int d = 0; d < sc.ndst; ++d)
+          __stcg(reinterpret_cast<int4*>(sc.dst[d] + e * (int64_t)sizeof(T)), packed);
+      }
+    }
+  }
+}
+
+template <typename T, int NSRC, int ACC>
+__device__ __forceinline__ void fold_scalar_acc(const SegCtx& sc, int64_t elem) {
+  using Tr = Traits<T>;
+  using Acc = typename Tr::Acc;
+  if constexpr (sizeof(Acc) == 4 && Tr::VEC == 8) {
+    FoldState<T, 1, 1> st;
+#pragma unroll
+    for (int j = 0; j < NSRC; ++j) {
+      Acc x[1];
+      if (ACC & 1)
+        x[0] = __ldcg(reinterpret_cast<const float*>(sc.src[j] + elem * 4));
+      else
+        x[0] = Tr::from_bits(__ldcg(reinterpret_cast<const typename Tr::Bits*>(sc.src[j] + elem * (int64_t)sizeof(T))));
+      st.feed(sc.ctrl[j], x);
+    }
+    for (int d = 0; d < sc.ndst; ++d) {
+      if (ACC & 2)
+        __stcg(reinterpret_cast<float*>(sc.dst[d] + elem * 4), st.result(0));
+      else
+        __stcg(reinterpret_cast<typename Tr::Bits*>(sc.dst[d] + elem * (int64_t)sizeof(T)), Tr::to_bits(st.result(0)));
+    }
+  }
+}
+
+#define RBX_ACC_SHAPES(X)                                                                                  \
+  X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
+
+template <typename T>
+__device__ __forceinline__ void dispatch_body_acc(int nsrc, int acc, const SegCtx& sc, int64_t body_off, int64_t v0,
+                                                  int64_t v1) {
+  if constexpr (sizeof(typename Traits<T>::Acc) == 4 && Traits<T>::VEC == 8) {
+    switch (nsrc * 4 + acc) {
+#define RBX_ACC_CASE(N)                                            \
+  case N * 4 + 1: fold_body_acc<T, N, 1>(sc, body_off, v0, v1); break; \
+  case N * 4 + 2: fold_body_acc<T, N, 2>(sc, body_off, v0, v1); break; \
+  case N * 4 + 3: fold_body_acc<T, N, 3>(sc, body_off, v0, v1); break;
+      RBX_ACC_SHAPES(RBX_ACC_CASE)
+#undef RBX_ACC_CASE
+      default: break;
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void dispatch_scalar_acc(int nsrc, int acc, const SegCtx& sc, int64_t elem) {
+  if constexpr (sizeof(typename Traits<T>::Acc) == 4 && Traits<T>::VEC == 8) {
+    switch (nsrc * 4 + acc) {
+#define RBX_ACC_CASE(N)                                 \
+  case N * 4 + 1: fold_scalar_acc<T, N, 1>(sc, elem); break; \
+  case N * 4 + 2: fold_scalar_acc<T, N, 2>(sc, elem); break; \
+  case N * 4 + 3: fold_scalar_acc<T, N, 3>(sc, elem); break;
+      RBX_ACC_SHAPES(RBX_ACC_CASE)
+#undef RBX_ACC_CASE
+      default: break;
+    }
+  }
+}
+
 // (operand count, nesting depth) pairs that grid factorizations of <= 16 ranks produce.
 #ifndef RBX_FOLD_SHAPES
 #define RBX_FOLD_SHAPES(X)                                                                              \
@@ -403,7 +522,10 @@ __device__ __forceinline__ void run_step_work(const Plan& P, const Step& st, int
           setup(k);
           s_cur = k;
         }
-        dispatch_body<T>(sg.nsrc, sg.nlev, s_seg, sg.body_off, a - sg.vec_begin, z - sg.vec_begin);
+        if (sg.acc)
+          dispatch_body_acc<T>(sg.nsrc, sg.acc, s_seg, sg.body_off, a - sg.vec_begin, z - sg.vec_begin);
+        else
+          dispatch_body<T>(sg.nsrc, sg.nlev, s_seg, sg.body_off, a - sg.vec_begin, z - sg.vec_begin);
       }
       ++k;
     }
@@ -427,7 +549,10 @@ __device__ __forceinline__ void run_step_work(const Plan& P, const Step& st, int
     }
     for (int i = threadIdx.x; i < sg.head + sg.tail; i += blockDim.x) {
       const int64_t elem = i < sg.head ? sg.off + i : sg.body_off + sg.nvec * P.vec + (i - sg.head);
-      dispatch_scalar<T>(sg.nsrc, sg.nlev, s_seg, elem);
+      if (sg.acc)
+        dispatch_scalar_acc<T>(sg.nsrc, sg.acc, s_seg, elem);
+      else
+        dispatch_scalar<T>(sg.nsrc, sg.nlev, s_seg, elem);
     }
   }
 }

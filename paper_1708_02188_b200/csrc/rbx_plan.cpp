@@ -208,6 +208,7 @@ struct SegProto {
   std::vector<uint8_t> ctrl;
   int nlev;
   std::vector<int> dst;
+  int acc = 0;  // Seg::acc
 };
 
 std::vector<uint8_t> single_level_ctrl(size_t n) {
@@ -257,6 +258,7 @@ static bool add_segments(Plan* p, std::vector<SegProto>& segs, int tbl, int vec,
     sg.nsrc = (uint8_t)sp.src.size();
     sg.ndst = (uint8_t)sp.dst.size();
     sg.nlev = (uint8_t)sp.nlev;
+    sg.acc = (uint8_t)sp.acc;
     for (size_t i = 0; i < sp.src.size(); ++i) {
       sg.src[i] = (uint8_t)sp.src[i];
       sg.ctrl[i] = sp.ctrl[i];
@@ -424,7 +426,22 @@ bool build_plan(const Geometry& g, int me, int64_t count, const PlanSpec& spec, 
         region(me, i + 1, &o, &l);
         std::vector<int> dst = {me};
         if (i == last && spec.op == OP_ALLREDUCE) dst = rotated_after(ring[i], me);
-        segs.push_back(SegProto{(int)steps.size(), o, l, rot_src(i), fold_ctrl1(i), 1, dst});
+        std::vector<int> src = rot_src(i);
+        int acc = 0;
+        if (spec.partials_fp32 && m > 1) {
+          // stage partials stay fp32 in the workspaces (one RNE at the very end)
+          if (i > 0) {
+            for (int& q : src) q += n;
+            acc |= 1;
+          }
+          if (i < last) {
+            dst = {n + me};
+            acc |= 2;
+          }
+        }
+        SegProto sp{(int)steps.size(), o, l, src, fold_ctrl1(i), 1, dst};
+        sp.acc = acc;
+        segs.push_back(sp);
         if (i < last)
           s.sigs = ring[i + 1];
         else
@@ -548,6 +565,7 @@ int64_t describe_plan(const Plan& p, int64_t* out, int64_t cap) {
       v.push_back(sg.head);
       v.push_back(sg.nvec);
       v.push_back(sg.tail);
+      v.push_back(sg.acc);
     }
   }
   const int64_t n = (int64_t)v.size();

@@ -56,7 +56,8 @@ struct Seg {
   int64_t nvec;            // body vectors
   int32_t head, tail;      // scalar elements before / after the body
   int32_t tbl;             // base index of this segment's buffer in the pointer table
-  uint8_t nsrc, ndst, nlev, pad;
+  uint8_t nsrc, ndst, nlev;
+  uint8_t acc;             // bit0: sources are fp32 partials, bit1: destinations are (bf16/f16 ring_dims)
   uint8_t src[RBX_MAX_RANKS];   // ranks, in fold order
   uint8_t dst[RBX_MAX_RANKS];   // ranks to store the result into
   uint8_t ctrl[RBX_MAX_RANKS];  // nested-fold control: bits0-3 "level L starts", bits4-5 levels passing up
@@ -133,6 +134,8 @@ struct PlanSpec {
   Op op = OP_ALLREDUCE;
   Mode mode = MODE_FUSED;
   int vec = 4;             // elements per 16B vector of the dtype
+  bool partials_fp32 = false;  // RING_DIMS with bf16/f16: inter-stage partials in fp32 workspaces
+                               // (table entries [R, 2R) = every rank's workspace)
   int mis = 0;             // (base address % 16) / itemsize, same on every rank; -1: never vectorise
   int64_t lo = 0, hi = -1; // element window [lo, hi) (hi < 0: whole buffer)
   int nblocks = 148;

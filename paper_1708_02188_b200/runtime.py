@@ -272,7 +272,11 @@ class RankContext:
         """MODE_PUSH needs a symmetric inbox (~1x the buffer bytes); grow it
         collectively when a larger buffer shows up (all ranks make the same
         calls with the same counts, so they grow together)."""
-        if mode != _native.MODES["push"] or op not in ("allreduce", "reduce_scatter", "buckets", "window"):
+        if op not in ("allreduce", "reduce_scatter", "buckets", "window"):
+            return
+        fp32_partials = (mode == _native.MODES["ring_dims"] and dtype in ("bf16", "f16")
+                         and sum(1 for d in self.grid.dims if d > 1) > 1)
+        if mode != _native.MODES["push"] and not fp32_partials:
             return
         need = _native.inbox_bytes(list(self.grid.dims), list(counts), dtype)
         if need <= self._inbox_bytes:

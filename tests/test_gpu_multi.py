@@ -219,6 +219,62 @@ def test_bucket_list_one_launch(world):
             assert digs[k] == orc.sha256(orc.closed_form_allreduce(orc.Grid(dims), parts))
 
 
+def _bf16_main(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1708_02188_b200.multiring import Grid
+    from paper_1708_02188_b200.runtime import RankContext
+
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = []
+        dims = (2, world // 2) if world >= 4 else (world,)
+        for mode in ("fused", "ring_dims", "push"):
+            ctx = RankContext(rank, Grid(dims), device=rank, mode=mode)
+            rng = np.random.default_rng(100 + rank)
+            bits = orc.bf16_round(rng.standard_normal(30_011).astype(np.float32))
+            t = ctx.empty(len(bits), "bf16")
+            t.copy_(torch.from_numpy(bits.view(np.int16)).view(torch.bfloat16))
+            ctx.collective("allreduce", t)
+            out.append((mode, hashlib.sha256(t.view(torch.int16).cpu().numpy().tobytes()).hexdigest()))
+            ctx.close()
+        q.put((rank, "ok", out))
+    except Exception as exc:  # noqa: BLE001
+        q.put((rank, "error", repr(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_bf16_all_modes_match_policy(world):
+    """bf16 (fp32 accumulate, one RNE): FUSED, RING_DIMS (fp32 partial
+    workspaces between stages) and PUSH all equal the oracle policy."""
+    if cuda_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_bf16_main, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    dims = (2, world // 2) if world >= 4 else (world,)
+    parts = [orc.bf16_round(np.random.default_rng(100 + r).standard_normal(30_011).astype(np.float32))
+             for r in range(world)]
+    want = orc.sha256(orc.bf16_allreduce(orc.Grid(dims), parts).view(np.int16))
+    for rank, status, out in res:
+        assert status == "ok", out
+        for mode, dig in out:
+            assert dig == want, (rank, mode)
+
+
 def _calib_main(rank, world, port, q):
     import torch
     import torch.distributed as dist

@@ -130,12 +130,6 @@ def test_bf16_f16_fp32_accumulate(mode):
         rng = np.random.default_rng(5)
         xs32 = [rng.standard_normal(33_333).astype(np.float32) for _ in range(n)]
         vr = VirtualRanks(dims, nblocks_per_rank=0 if mode == "local" else 4)
-        if mode == "ring_dims":
-            ts = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in xs32]
-            with pytest.raises(NotImplementedError):
-                vr.collective(ts, mode=mode)
-            vr.close()
-            continue
         bits = [orc.bf16_round(x) for x in xs32]
         ts = [torch.from_numpy(b.view(np.int16)).cuda().view(torch.bfloat16) for b in bits]
         vr.collective(ts, mode=mode)
