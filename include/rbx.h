@@ -42,13 +42,16 @@ extern "C" {
 #define RBX_I32 5
 
 /* execution modes (all produce bit-identical results) */
-#define RBX_MODE_AUTO 0       /* = FUSED */
+#define RBX_MODE_AUTO 0       /* LL for a whole-buffer allreduce of <= RBX_LL_AUTO_BYTES (env, default
+                                 1 MiB) on a multi-GPU communicator, else FUSED */
 #define RBX_MODE_RING_DIMS 1  /* one reduce-scatter / all-gather stage per grid dimension (the paper's rings) */
 #define RBX_MODE_FUSED 2      /* all dims folded in one pass (nested order), result pushed to every peer */
 #define RBX_MODE_FUSED_PULL 3 /* like FUSED, but the all-gather pulls the peers' owned chunks */
 #define RBX_MODE_LOCAL 4      /* virtual ranks on one GPU, no synchronisation (1-GPU roofline) */
 #define RBX_MODE_PUSH 5       /* two-shot, NVLink writes only: inputs pushed to the owners' inboxes
                                  (rbx_set_inbox), results pushed back to every rank */
+#define RBX_MODE_LL 6         /* low latency, allreduce of <= 1 MiB per rank: 8-byte {data, epoch} words
+                                 pushed into the communicator's LL area, no flags or fences */
 
 /* collective ops */
 #define RBX_OP_ALLREDUCE 0

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("RBX_LIB_PATH") or os.path.join(_HERE, "librbx.so")  #
 OK, ERR_INVALID, ERR_CUDA, ERR_COLLECTIVE, ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 DTYPE_CODES = {"f32": 0, "f64": 1, "i64": 2, "bf16": 3, "f16": 4, "i32": 5}
 ITEMSIZE = {"f32": 4, "f64": 8, "i64": 8, "bf16": 2, "f16": 2, "i32": 4}
-MODES = {"auto": 0, "ring_dims": 1, "fused": 2, "fused_pull": 3, "local": 4, "push": 5}
+MODES = {"auto": 0, "ring_dims": 1, "fused": 2, "fused_pull": 3, "local": 4, "push": 5, "ll": 6}
 OPS = {"allreduce": 0, "reduce_scatter": 1, "allgather": 2, "barrier": 3}
 
 

@@ -24,6 +24,7 @@
 #include "rbx_plan.h"
 
 #include "rbx_local.cuh"
+#include "rbx_ll.cuh"
 
 namespace rbx {
 const void* local_kernel_f32(int v, int nlev);
@@ -38,6 +39,12 @@ const void* step_kernel_i64();
 const void* step_kernel_bf16();
 const void* step_kernel_f16();
 const void* step_kernel_i32();
+const void* ll_kernel_f32();
+const void* ll_kernel_f64();
+const void* ll_kernel_i64();
+const void* ll_kernel_bf16();
+const void* ll_kernel_f16();
+const void* ll_kernel_i32();
 }  // namespace rbx
 
 namespace {
@@ -121,6 +128,16 @@ struct rbx_comm {
   size_t inbox_bytes = 0;
   std::vector<char*> inbox_at;
   bool inbox_owned = false;  // virtual comms allocate their own
+  // MODE_LL: every rank's LL area (rbx_ll.cuh), carved from the signal allocation
+  std::vector<unsigned long long*> ll_at;
+  size_t ll_auto_bytes = RBX_LL_MAX_BYTES;  // AUTO picks LL up to this many bytes per rank; env RBX_LL_AUTO_BYTES
+  int ll_threads = 512;
+  // one-shot LL up to this many bytes; env RBX_LL_ONESHOT_BYTES.  Off by default: on B200 it
+  // measured slower than two-shot at every size (4 KB: 21 vs 13 us event time at N=2,
+  // profiles/r01_ll_*), the launch/teardown floor dominates and it folds N x the elements.
+  int64_t ll_oneshot_bytes = 0;
+  int ll_words_per_thread = 4;        // CTAs per LL call = words / (threads * this); env RBX_LL_WPT
+  int ll_coresident = 0;              // co-resident CTAs of the LL kernel
 };
 
 namespace {
@@ -158,6 +175,26 @@ const void* kernel_for(int dtype) {
     case RBX_I32: return rbx::step_kernel_i32();
     default: return nullptr;
   }
+}
+
+const void* ll_kernel_for(int dtype) {
+  switch (dtype) {
+    case RBX_F32: return rbx::ll_kernel_f32();
+    case RBX_F64: return rbx::ll_kernel_f64();
+    case RBX_I64: return rbx::ll_kernel_i64();
+    case RBX_BF16: return rbx::ll_kernel_bf16();
+    case RBX_F16: return rbx::ll_kernel_f16();
+    case RBX_I32: return rbx::ll_kernel_i32();
+    default: return nullptr;
+  }
+}
+
+// One allocation per rank holds the signal area and, 256-byte aligned after
+// it, the LL area; both are exported with one IPC handle.
+constexpr size_t ll_offset() { return ((size_t)rbx::SigLayout::bytes + 255) / 256 * 256; }
+size_t sig_alloc_bytes(int nranks) { return ll_offset() + (size_t)rbx::ll_area_bytes(nranks); }
+unsigned long long* ll_area_of(uint32_t* sig) {
+  return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(sig) + ll_offset());
 }
 
 const void* local_kernel_for(int dtype, int v, int nlev) {
@@ -230,6 +267,10 @@ int common_init(rbx_comm* c, const int* dims, int ndims, int device, int threads
   if (const char* t = std::getenv("RBX_LOCAL_GENERIC")) c->local_specialised = std::atoi(t) == 0;
   if (const char* t = std::getenv("RBX_BYTES_PER_CTA")) c->bytes_per_cta = (size_t)std::max(1L, std::atol(t));
   if (const char* t = std::getenv("RBX_MIN_BLOCKS")) c->min_blocks = std::max(1, std::atoi(t));
+  if (const char* t = std::getenv("RBX_LL_AUTO_BYTES"))
+    c->ll_auto_bytes = std::min((size_t)std::max(0L, std::atol(t)), (size_t)RBX_LL_MAX_BYTES);
+  if (const char* t = std::getenv("RBX_LL_WPT")) c->ll_words_per_thread = std::max(1, std::atoi(t));
+  if (const char* t = std::getenv("RBX_LL_ONESHOT_BYTES")) c->ll_oneshot_bytes = std::atol(t);
   RBX_CUDA(cudaSetDevice(device));
   RBX_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
   int rc = coresident_blocks(device, threads, &c->max_coresident);
@@ -312,7 +353,75 @@ int launch(rbx_comm* c, const CachedPlan& cp, int dtype, cudaStream_t stream, bo
 // silently round partials (parity policy: one RNE at the end).
 int check_mode_dtype(int mode, int dtype) {
   (void)dtype;
-  if (mode < RBX_MODE_AUTO || mode > RBX_MODE_PUSH) return fail(RBX_ERR_INVALID, "unknown mode");
+  if (mode < RBX_MODE_AUTO || mode > RBX_MODE_LL) return fail(RBX_ERR_INVALID, "unknown mode");
+  return RBX_OK;
+}
+
+// MODE_LL launch (rbx_ll.cuh): ranks[0..nhosted) are the ranks this launch
+// plays (1 for a per-rank communicator, V for a virtual one).
+int ll_launch(rbx_comm* c, const std::vector<int>& ranks, void* const* bufs, size_t count, int dtype,
+              cudaStream_t stream, bool cooperative) {
+  const void* fn = ll_kernel_for(dtype);
+  if (!fn) return fail(RBX_ERR_INVALID, "unknown dtype");
+  const int es = dtype_size(dtype);
+  if (count * (size_t)es > (size_t)RBX_LL_MAX_BYTES)
+    return fail(RBX_ERR_INVALID, "MODE_LL handles at most " + std::to_string(RBX_LL_MAX_BYTES) + " bytes per rank");
+  if (c->ll_coresident == 0) {
+    int per_sm = 0;
+    RBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, c->ll_threads, 0));
+    c->ll_coresident = std::max(1, per_sm) * c->sm_count;
+  }
+  const rbx::Geometry& g = c->geo;
+  const int m = (int)g.active_dims().size();
+  const int W = es == 8 ? 2 : 1;
+  const int64_t words = (int64_t)count * W;
+  int nb = (int)std::min<int64_t>((words + (int64_t)c->ll_threads * c->ll_words_per_thread - 1) /
+                                      ((int64_t)c->ll_threads * c->ll_words_per_thread),
+                                  (int64_t)c->nblocks);
+  if (nb < 1) nb = 1;
+  const int V = (int)ranks.size();
+  if ((int64_t)nb * V > c->ll_coresident) nb = std::max(1, c->ll_coresident / V);
+  std::unique_ptr<rbx::LLArgs> a(new rbx::LLArgs);
+  std::memset(a.get(), 0, sizeof(rbx::LLArgs));
+  a->nranks = c->nranks;
+  a->nlev = m;
+  a->nb = nb;
+  a->nhosted = V;
+  a->cap = rbx::ll_cap_words(c->nranks);
+  a->timeout_ns = c->timeout_ns;
+  a->err = c->err_dev;
+  a->trace = c->trace_dev;
+  const int64_t bytes = (int64_t)count * es;
+  a->oneshot = bytes <= c->ll_oneshot_bytes && bytes <= RBX_LL_ONESHOT_MAX_BYTES;
+  for (int q = 0; q < c->nranks; ++q) {
+    const std::vector<int> o = rbx::fold_order(g, q);
+    for (int k = 0; k < c->nranks; ++k) a->orders.of[q][k] = (uint8_t)o[k];
+  }
+  const std::vector<uint8_t> ctrl = rbx::fold_ctrl(g);
+  for (int v = 0; v < V; ++v) {
+    rbx::LLRank& R = a->rank[v];
+    const int me = ranks[v];
+    R.me = me;
+    R.buf = static_cast<char*>(bufs[v]);
+    R.my_sig = c->sig[me];
+    for (int q = 0; q < c->nranks; ++q) {
+      R.area[q] = c->ll_at[q];
+      rbx::region_after(g, q, (int64_t)count, m, &R.off[q], &R.len[q]);
+    }
+    const std::vector<int> order = rbx::fold_order(g, me);
+    for (int k = 0; k < c->nranks; ++k) {
+      R.order[k] = (uint8_t)order[k];
+      R.ctrl[k] = ctrl[k];
+    }
+  }
+  void* params[] = {a.get()};
+  dim3 grid((unsigned)(nb * V)), block((unsigned)c->ll_threads);
+  if (cooperative) {
+    RBX_CUDA(cudaLaunchCooperativeKernel(fn, grid, block, params, 0, stream));
+  } else {
+    RBX_CUDA(cudaLaunchKernel(fn, grid, block, params, 0, stream));
+  }
+  c->launches++;
   return RBX_OK;
 }
 
@@ -405,6 +514,15 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
   size_t total = 0;
   for (int k = 0; k < nbufs; ++k) total += counts[k];
   if (total == 0 && op != RBX_OP_BARRIER) return RBX_OK;  // empty collective: nothing moves on any rank
+  const bool whole = lo == 0 && (hi < 0 || hi == (int64_t)total);
+  if (mode == RBX_MODE_LL) {
+    if (op != RBX_OP_ALLREDUCE || nbufs != 1 || !whole)
+      return fail(RBX_ERR_INVALID, "MODE_LL supports a whole-buffer single allreduce only");
+    return ll_launch(c, {c->rank}, bufs, counts[0], dtype, stream, false);
+  }
+  if (mode == RBX_MODE_AUTO && op == RBX_OP_ALLREDUCE && nbufs == 1 && whole && c->nranks > 1 &&
+      total * (size_t)es <= c->ll_auto_bytes)
+    return ll_launch(c, {c->rank}, bufs, counts[0], dtype, stream, false);
   std::vector<const void*> kp(bufs, bufs + nbufs);
   std::vector<size_t> kc(counts, counts + nbufs);
   const std::string key = plan_key(op, mode, dtype, kp, kc) + "@" + std::to_string(lo) + ":" + std::to_string(hi);
@@ -606,13 +724,15 @@ int rbx_comm_create(rbx_comm_t** comm, int rank, int nranks, const int* dims, in
   if (nblocks > RBX_MAX_BLOCKS) nblocks = RBX_MAX_BLOCKS;
   if (nblocks > c->max_coresident) nblocks = c->max_coresident;  // deadlock freedom: all CTAs resident
   c->nblocks = nblocks;
-  RBX_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->sig_local), rbx::SigLayout::bytes));
-  RBX_CUDA(cudaMemset(c->sig_local, 0, rbx::SigLayout::bytes));
+  RBX_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->sig_local), sig_alloc_bytes(nranks)));
+  RBX_CUDA(cudaMemset(c->sig_local, 0, sig_alloc_bytes(nranks)));
   cudaIpcMemHandle_t h;
   RBX_CUDA(cudaIpcGetMemHandle(&h, c->sig_local));
   std::memcpy(signal_handle->bytes, &h, sizeof(h));
   c->sig.assign(nranks, nullptr);
   c->sig[rank] = c->sig_local;
+  c->ll_at.assign(nranks, nullptr);
+  c->ll_at[rank] = ll_area_of(c->sig_local);
   RBX_CUDA(cudaDeviceSynchronize());
   *comm = c.release();
   return RBX_OK;
@@ -627,6 +747,7 @@ int rbx_comm_connect(rbx_comm_t* c, const rbx_ipc_handle_t* handles) {
     int rc = open_handle(handles[q], &p);
     if (rc) return rc;
     c->sig[q] = static_cast<uint32_t*>(p);
+    c->ll_at[q] = ll_area_of(c->sig[q]);
     c->opened_sig.push_back(p);
   }
   c->connected = true;
@@ -815,10 +936,15 @@ int rbx_vcomm_create(rbx_comm_t** comm, int nranks, const int* dims, int ndims, 
   if (nb < 1) nb = 1;
   if (nb > RBX_MAX_BLOCKS) nb = RBX_MAX_BLOCKS;
   c->nblocks = nb;
-  RBX_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->sig_local), rbx::SigLayout::bytes * nranks));
-  RBX_CUDA(cudaMemset(c->sig_local, 0, rbx::SigLayout::bytes * nranks));
+  const size_t stride = sig_alloc_bytes(nranks);  // per virtual rank: signal area + LL area
+  RBX_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->sig_local), stride * nranks));
+  RBX_CUDA(cudaMemset(c->sig_local, 0, stride * nranks));
   c->sig.resize(nranks);
-  for (int q = 0; q < nranks; ++q) c->sig[q] = c->sig_local + q * rbx::SigLayout::words;
+  c->ll_at.resize(nranks);
+  for (int q = 0; q < nranks; ++q) {
+    c->sig[q] = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(c->sig_local) + stride * q);
+    c->ll_at[q] = ll_area_of(c->sig[q]);
+  }
   c->connected = true;
   RBX_CUDA(cudaDeviceSynchronize());
   *comm = c.release();
@@ -847,6 +973,14 @@ int rbx_vcollective_window(rbx_comm_t* c, void* const* bufs, size_t count, size_
   if (c->err_host->code) return fail(RBX_ERR_COLLECTIVE, "communicator is in an error state", c->err_host->peer, c->err_host->step);
   if (int rc = check_mode_dtype(mode, dtype)) return rc;
   const int V = c->nvirtual;
+  if (mode == RBX_MODE_LL) {
+    if (op != RBX_OP_ALLREDUCE || lo != 0 || hi != count)
+      return fail(RBX_ERR_INVALID, "MODE_LL supports a whole-buffer single allreduce only");
+    if (count == 0) return RBX_OK;
+    std::vector<int> ranks;
+    for (int r = 0; r < V; ++r) ranks.push_back(r);
+    return ll_launch(c, ranks, bufs, count, dtype, (cudaStream_t)stream, true);
+  }
   std::vector<const void*> kp(bufs, bufs + V);
   const std::string key =
       plan_key(op, mode, dtype, kp, {count}) + "@" + std::to_string(lo) + ":" + std::to_string(hi);

@@ -2,9 +2,11 @@
 // kernel and the specialised local-reduce kernels.
 #include "rbx_kernel.cuh"
 #include "rbx_local.cuh"
+#include "rbx_ll.cuh"
 
 namespace rbx {
 const void* step_kernel_i64() { return reinterpret_cast<const void*>(&rbx_step_kernel<unsigned long long>); }
+const void* ll_kernel_i64() { return reinterpret_cast<const void*>(&rbx_ll_kernel<unsigned long long>); }
 
 const void* local_kernel_i64(int v, int nlev) {
 #define RBX_LOCAL_CASE(V, L) \

@@ -1,0 +1,342 @@
+// Low-latency (LL) allreduce for small messages: one launch, no flags, no
+// fences, no entry barrier.
+//
+// Every datum travels as one 8-byte word {payload u32, epoch u32} stored with a
+// single 64-bit relaxed.sys store, which is single-copy atomic, so a receiver
+// that sees the current epoch in the upper half also sees the payload: the
+// data carries its own ready flag.  That removes the st.release.sys /
+// ld.acquire.sys pair (~4 us of fence per step on B200, tools/entry_probe.cu)
+// and the ENTRY handshake: no peer ever touches this rank's buffer.
+//
+//   1. scatter: every element of peer q's owned region goes into q's LL area,
+//      slot [me] (one word per 2/4-byte element, two per 8-byte element);
+//   2. fold: for my owned region, fold my buffer and the N-1 slots in the
+//      reference order (FUSED's nested rotated fold, rbx_plan.cpp fold_order /
+//      fold_ctrl) -- bit-identical to every other mode; store the result into
+//      my buffer and push it as LL words into every peer's gather slot [me];
+//   3. gather: copy every peer's owned result from my gather slots.
+//
+// ONE-SHOT variant (tiny buffers, and N = 2 where it moves the same bytes):
+// every rank pushes its whole buffer to every peer and then folds EVERY
+// element itself, each owned region in its owner's reference order, so all
+// ranks compute the same bits with one NVLink hop instead of two.  Its slots
+// are double-buffered by epoch parity: rank r can only be one launch ahead of
+// a peer that has not finished reading (r's launch e+1 needs that peer's
+// words of launch e+1, sent after the peer's launch e completed).
+//
+// Slot reuse needs no credits: rank r's next launch starts only after this one
+// saw every owner's result for every element, and an owner produces element
+// i's result only after reading r's word i.  Allreduce only (reduce-scatter
+// alone would break that argument).
+//
+// Reference mapping: one LL launch = the whole phase loop of _run_phases
+// (pkg/src/ringbox/runtime.py:199-267) for a small buffer; the epoch in every
+// word plays the role of the frame header check (runtime.py:229-245).
+#pragma once
+#include "rbx_kernel.cuh"
+
+namespace rbx {
+
+#define RBX_LL_MAX_BYTES (1 << 20)       // per-rank payload cap of two-shot LL (bytes of the user buffer)
+#define RBX_LL_ONESHOT_MAX_BYTES (1 << 16)  // per-rank payload cap of one-shot LL
+
+// LL area of one rank (u64 words): two-shot scatter[R][cap] and gather[R][cap],
+// then one-shot slots[2 parities][R][cap1].
+__host__ __device__ inline int64_t ll_cap_words(int nranks) {
+  return (RBX_LL_MAX_BYTES / 2 + nranks - 1) / nranks + 16;
+}
+__host__ __device__ inline int64_t ll_cap1_words() { return RBX_LL_ONESHOT_MAX_BYTES / 2; }
+__host__ __device__ inline int64_t ll_oneshot_off(int nranks) { return 2 * (int64_t)nranks * ll_cap_words(nranks); }
+__host__ __device__ inline int64_t ll_area_bytes(int nranks) {
+  return (ll_oneshot_off(nranks) + 2 * (int64_t)nranks * ll_cap1_words()) * 8;
+}
+
+struct LLRank {
+  char* buf;                            // this rank's buffer (only this rank touches it)
+  unsigned long long* area[RBX_MAX_RANKS];  // every rank's LL area, mapped ([me] = own)
+  uint32_t* my_sig;                     // epoch word, done counter, abort word
+  int64_t off[RBX_MAX_RANKS], len[RBX_MAX_RANKS];  // owned regions (elements)
+  uint8_t order[RBX_MAX_RANKS], ctrl[RBX_MAX_RANKS];  // fold order of my region
+  int me;
+};
+
+struct LLOrders {  // one-shot: the fold order of every owner's region
+  uint8_t of[RBX_MAX_RANKS][RBX_MAX_RANKS];
+};
+
+struct LLArgs {
+  int nranks, nlev, nb;  // nb CTAs per rank
+  int nhosted;           // ranks hosted by this launch (1, or V for a virtual communicator)
+  int oneshot;           // 1: one-shot variant
+  int64_t cap;           // words per slot
+  uint64_t timeout_ns;
+  ErrRecord* err;
+  unsigned long long* trace;  // optional timeline (RBX_TRACE), same slots as rbx_step_kernel
+  LLOrders orders;
+  LLRank rank[RBX_MAX_RANKS];
+};
+
+__device__ __forceinline__ void st_ll(unsigned long long* p, uint32_t data, uint32_t e) {
+  const unsigned long long v = ((unsigned long long)e << 32) | data;
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_ll(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// word w of element range starting at element `o` of a buffer of T
+template <typename T>
+__device__ __forceinline__ uint32_t ll_load_word(const char* buf, int64_t o, int64_t w) {
+  if (sizeof(T) == 2) return (uint32_t)__ldcg(reinterpret_cast<const unsigned short*>(buf) + o + w);
+  return __ldcg(reinterpret_cast<const unsigned int*>(buf + o * (int64_t)sizeof(T)) + w);
+}
+template <typename T>
+__device__ __forceinline__ void ll_store_word(char* buf, int64_t o, int64_t w, uint32_t v) {
+  if (sizeof(T) == 2)
+    reinterpret_cast<unsigned short*>(buf)[o + w] = (unsigned short)v;
+  else
+    reinterpret_cast<unsigned int*>(buf + o * (int64_t)sizeof(T))[w] = v;
+}
+
+struct LLWait {
+  uint32_t e;
+  uint64_t t0, timeout_ns;
+  volatile uint32_t* abort_word;
+  bool failed;
+  // payload of the word at p once its epoch is current; false on timeout/abort
+  __device__ __forceinline__ uint32_t get(const unsigned long long* p) {
+    uint32_t it = 0;
+    while (true) {
+      const unsigned long long v = ld_ll(p);
+      if ((uint32_t)(v >> 32) == e) return (uint32_t)v;
+      if (failed) return 0;
+      if ((++it & 1023u) == 0) {
+        if (*abort_word || global_ns() - t0 > timeout_ns) {
+          failed = true;
+          return 0;
+        }
+      }
+    }
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ typename Traits<T>::Acc ll_value(uint32_t lo, uint32_t hi) {
+  using B = typename Traits<T>::Bits;
+  if (sizeof(T) == 8) return Traits<T>::from_bits((B)(((unsigned long long)hi << 32) | lo));
+  return Traits<T>::from_bits((B)lo);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512) rbx_ll_kernel(const __grid_constant__ LLArgs a) {
+  using Acc = typename Traits<T>::Acc;
+  constexpr int W = sizeof(T) == 8 ? 2 : 1;  // LL words per element
+  constexpr int U = 4;                       // words per thread in flight (phases 1 and 3)
+  const int v = blockIdx.x / a.nb, b = blockIdx.x % a.nb;
+  const LLRank& R = a.rank[v];
+  const int N = a.nranks, me = R.me;
+  const int64_t cap = a.cap;
+  __shared__ uint32_t s_epoch;
+  __shared__ int s_fail;
+  // timeline of thread 0 of the first and last CTA of the first hosted rank:
+  // [0] start [1] epoch read [3] pushed [4] folded [5] gathered [30] done [31] exit
+  unsigned long long* tr = nullptr;
+  if (a.trace && threadIdx.x == 0 && v == 0 && (b == 0 || b == a.nb - 1)) tr = a.trace + (b == 0 ? 0 : 32);
+  if (tr) {
+    tr[29] = tr[31];
+    tr[0] = global_ns();
+  }
+  if (threadIdx.x == 0) {
+    s_epoch = *(volatile uint32_t*)(R.my_sig + SigLayout::epoch_off) + 1u;
+    s_fail = 0;
+  }
+  __syncthreads();
+  LLWait wt{s_epoch, global_ns(), a.timeout_ns, (volatile uint32_t*)(R.my_sig + SigLayout::abort_off), false};
+  if (tr) tr[1] = global_ns();
+  const uint32_t e = wt.e;
+  const int64_t tid = (int64_t)b * blockDim.x + threadIdx.x, nthr = (int64_t)a.nb * blockDim.x;
+  unsigned long long* own = R.area[me];
+
+  if (a.oneshot) {
+    // my whole buffer -> every peer's slot [parity][me]; then fold every element.
+    // The same thread pushes and folds element i (it overwrites buf[i] last).
+    const int64_t par = (int64_t)(e & 1u) * N * ll_cap1_words();
+    for (int q = 0; q < N; ++q) {
+      const int64_t o = R.off[q], n = R.len[q];
+      for (int64_t i = tid; i < n; i += nthr) {
+        uint32_t mine[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) mine[j] = ll_load_word<T>(R.buf, o, i * W + j);
+        for (int k = 1; k < N; ++k) {
+          unsigned long long* dst = R.area[(me + k) % N] + ll_oneshot_off(N) + par + (int64_t)me * ll_cap1_words() +
+                                    (o + i) * W;
+#pragma unroll
+          for (int j = 0; j < W; ++j) st_ll(dst + j, mine[j], e);
+        }
+      }
+    }
+    if (tr) tr[3] = global_ns();
+    const unsigned long long* slots = own + ll_oneshot_off(N) + par;
+    for (int q = 0; q < N; ++q) {
+      const int64_t o = R.off[q], n = R.len[q];
+      for (int64_t i = tid; i < n; i += nthr) {
+        unsigned long long raw[RBX_MAX_RANKS][W];
+#pragma unroll
+        for (int k = 0; k < RBX_MAX_RANKS; ++k) {
+          if (k < N) {
+            const int p = a.orders.of[q][k];
+#pragma unroll
+            for (int j = 0; j < W; ++j)
+              raw[k][j] = p == me ? (((unsigned long long)e << 32) | ll_load_word<T>(R.buf, o, i * W + j))
+                                  : ld_ll(slots + (int64_t)p * ll_cap1_words() + (o + i) * W + j);
+          }
+        }
+        FoldState<T, 1, RBX_MAX_LEVELS> f;
+#pragma unroll
+        for (int k = 0; k < RBX_MAX_RANKS; ++k) {
+          if (k < N) {
+            const int p = a.orders.of[q][k];
+            uint32_t x2[W];
+#pragma unroll
+            for (int j = 0; j < W; ++j)
+              x2[j] = (uint32_t)(raw[k][j] >> 32) == e
+                          ? (uint32_t)raw[k][j]
+                          : wt.get(slots + (int64_t)p * ll_cap1_words() + (o + i) * W + j);
+            const Acc x[1] = {ll_value<T>(x2[0], x2[W - 1])};
+            f.feed(R.ctrl[k], x);
+          }
+        }
+        Acc r = f.a[0][0];
+#pragma unroll
+        for (int L = 1; L < RBX_MAX_LEVELS; ++L)
+          if (L == a.nlev - 1) r = f.a[L][0];
+        const unsigned long long bits = (unsigned long long)Traits<T>::to_bits(r);
+        const uint32_t rw[2] = {(uint32_t)bits, (uint32_t)(bits >> 32)};
+        if (!wt.failed) {
+#pragma unroll
+          for (int j = 0; j < W; ++j) ll_store_word<T>(R.buf, o, i * W + j, rw[j]);
+        }
+      }
+    }
+    if (tr) tr[4] = tr[5] = global_ns();
+  } else {
+  // 1. scatter my input of every peer's region into that peer's slot [me]
+  for (int k = 1; k < N; ++k) {
+    const int q = (me + k) % N;
+    const int64_t o = R.off[q], nw = R.len[q] * W;
+    unsigned long long* dst = R.area[q] + (int64_t)me * cap;
+    for (int64_t w0 = tid; w0 < nw; w0 += nthr * U) {
+      uint32_t d[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t w = w0 + u * nthr;
+        d[u] = w < nw ? ll_load_word<T>(R.buf, o, w) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t w = w0 + u * nthr;
+        if (w < nw) st_ll(dst + w, d[u], e);
+      }
+    }
+  }
+
+  if (tr) tr[3] = global_ns();
+  // 2. fold my region in the reference order; result -> my buffer + every peer's gather slot [me]
+  {
+    const int64_t o = R.off[me], n = R.len[me];
+    for (int64_t i = tid; i < n; i += nthr) {
+      // issue every source's word(s) at once, then re-poll the ones not yet current
+      unsigned long long raw[RBX_MAX_RANKS][W];
+#pragma unroll
+      for (int k = 0; k < RBX_MAX_RANKS; ++k) {
+        if (k < N) {
+          const int p = R.order[k];
+#pragma unroll
+          for (int j = 0; j < W; ++j) {
+            raw[k][j] = p == me ? (((unsigned long long)e << 32) | ll_load_word<T>(R.buf, o, i * W + j))
+                                : ld_ll(own + (int64_t)p * cap + i * W + j);
+          }
+        }
+      }
+      FoldState<T, 1, RBX_MAX_LEVELS> f;
+#pragma unroll
+      for (int k = 0; k < RBX_MAX_RANKS; ++k) {
+        if (k < N) {
+          const int p = R.order[k];
+          uint32_t x2[W];
+#pragma unroll
+          for (int j = 0; j < W; ++j)
+            x2[j] = (uint32_t)(raw[k][j] >> 32) == e ? (uint32_t)raw[k][j]
+                                                      : wt.get(own + (int64_t)p * cap + i * W + j);
+          const Acc x[1] = {ll_value<T>(x2[0], x2[W - 1])};
+          f.feed(R.ctrl[k], x);
+        }
+      }
+      Acc r = f.a[0][0];
+#pragma unroll
+      for (int L = 1; L < RBX_MAX_LEVELS; ++L)
+        if (L == a.nlev - 1) r = f.a[L][0];
+      const unsigned long long bits = (unsigned long long)Traits<T>::to_bits(r);
+      const uint32_t rw[2] = {(uint32_t)bits, (uint32_t)(bits >> 32)};
+#pragma unroll
+      for (int j = 0; j < W; ++j) ll_store_word<T>(R.buf, o, i * W + j, rw[j]);
+      for (int k = 1; k < N; ++k) {
+        unsigned long long* dst = R.area[(me + k) % N] + (int64_t)(N + me) * cap + i * W;
+#pragma unroll
+        for (int j = 0; j < W; ++j) st_ll(dst + j, rw[j], e);
+      }
+    }
+  }
+
+  if (tr) tr[4] = global_ns();
+  // 3. gather every peer's result from my gather slots
+  for (int k = 1; k < N; ++k) {
+    const int q = (me + k) % N;
+    const int64_t o = R.off[q], nw = R.len[q] * W;
+    const unsigned long long* src = own + (int64_t)(N + q) * cap;
+    for (int64_t w0 = tid; w0 < nw; w0 += nthr * U) {
+      unsigned long long raw[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t w = w0 + u * nthr;
+        raw[u] = w < nw ? ld_ll(src + w) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t w = w0 + u * nthr;
+        if (w < nw) {
+          const uint32_t d = (uint32_t)(raw[u] >> 32) == e ? (uint32_t)raw[u] : wt.get(src + w);
+          if (!wt.failed) ll_store_word<T>(R.buf, o, w, d);
+        }
+      }
+    }
+  }
+
+  if (tr) tr[5] = global_ns();
+  }  // two-shot
+
+  if (tr) tr[30] = global_ns();
+  if (wt.failed) s_fail = 1;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  if (s_fail) {
+    if (atomicCAS(&a.err->code, 0, 3) == 0) {
+      a.err->rank = me;
+      a.err->step = 0;
+      a.err->peer = -1;
+    }
+    *wt.abort_word = 1u;
+    return;  // the epoch is not advanced: the communicator is in an error state
+  }
+  // the last CTA of this rank publishes the epoch (same protocol as rbx_step_kernel)
+  unsigned int* done = reinterpret_cast<unsigned int*>(R.my_sig + SigLayout::epoch_off + 1);
+  if (atomicAdd(done, 1u) == (unsigned)a.nb - 1u) {
+    *done = 0u;
+    *(volatile uint32_t*)(R.my_sig + SigLayout::epoch_off) = e;
+  }
+  if (tr) tr[31] = global_ns();
+}
+
+}  // namespace rbx

@@ -70,6 +70,13 @@ def test_handle_exchange_world2():
         assert status == "ok" and firsts == [0, 1] and offs == [0, 4096]
 
 
+def test_handle_exchange_world8():
+    """The N=8 (2,2,2) bench/scale launch: every rank sees all 8 handles in rank order."""
+    res = _run("handles", world=8)
+    for rank, status, firsts, offs in res:
+        assert status == "ok" and firsts == list(range(8)) and offs == [r * 4096 for r in range(8)]
+
+
 def test_agreement_world2():
     assert all(r[1] == "ok" and r[2] == 2 for r in _run("agree"))
 

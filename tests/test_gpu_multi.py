@@ -101,7 +101,7 @@ def test_all_decompositions_all_modes_bit_exact(world):
     lengths = [0, 1, 17, 1000, 4099]
     cases = []
     for dims in _dims_for(world):
-        for mode in ("fused", "fused_pull", "ring_dims", "push"):
+        for mode in ("fused", "fused_pull", "ring_dims", "push", "ll"):
             for dtype in ("f32", "i64", "f64"):
                 cases.append({"dims": dims, "mode": mode, "dtype": dtype, "lengths": lengths, "seed": world})
     res = _spawn(world, cases)
@@ -232,7 +232,7 @@ def _bf16_main(rank, world, port, q):
     try:
         out = []
         dims = (2, world // 2) if world >= 4 else (world,)
-        for mode in ("fused", "ring_dims", "push"):
+        for mode in ("fused", "ring_dims", "push", "ll"):
             ctx = RankContext(rank, Grid(dims), device=rank, mode=mode)
             rng = np.random.default_rng(100 + rank)
             bits = orc.bf16_round(rng.standard_normal(30_011).astype(np.float32))

@@ -50,7 +50,7 @@ def run(vr, parts, op, mode, dtype_t):
     return [t.cpu().numpy() for t in ts]
 
 
-@pytest.mark.parametrize("mode", ["local", "fused", "fused_pull", "ring_dims", "push"])
+@pytest.mark.parametrize("mode", ["local", "fused", "fused_pull", "ring_dims", "push", "ll"])
 def test_all_decompositions_bit_exact(mode):
     """tests/golden/replay_digests.json: reference acceptance sweep
     (pkg/tests/test_acceptance.py:41-73) on the GPU, f32/f64/i64."""
@@ -117,7 +117,7 @@ def test_reduce_scatter_then_allgather(mode):
         vr.close()
 
 
-@pytest.mark.parametrize("mode", ["local", "fused", "ring_dims", "push"])
+@pytest.mark.parametrize("mode", ["local", "fused", "ring_dims", "push", "ll"])
 def test_bf16_f16_fp32_accumulate(mode):
     """bf16/f16: fold fp32-upcast inputs in the reference order, one RNE at the
     end (parity unpinned by the reference, which has no bf16: runtime.py:37)."""
@@ -163,7 +163,7 @@ def test_repeated_calls_epochs_and_launch_count():
         length = int(rng.integers(1, 50_000))
         parts = [rng.integers(-1000, 1001, length).astype(np.int64) for _ in range(8)]
         ts = [torch.from_numpy(p).cuda() for p in parts]
-        mode = ["fused", "ring_dims", "fused_pull", "push"][k % 4]
+        mode = ["fused", "ring_dims", "fused_pull", "push", "ll"][k % 5]
         vr.collective(ts, mode=mode)
         torch.cuda.synchronize()
         vr.check()
@@ -172,6 +172,61 @@ def test_repeated_calls_epochs_and_launch_count():
             assert np.array_equal(t.cpu().numpy(), want)
     assert vr.launches - base == 12
     vr.close()
+
+
+@pytest.mark.parametrize("oneshot_bytes", ["0", "65536"])
+def test_ll_oneshot_and_twoshot_variants(oneshot_bytes, monkeypatch):
+    """MODE_LL's two variants (RBX_LL_ONESHOT_BYTES=0 forces two-shot; 65536
+    makes every size here one-shot) against the reference replay digests."""
+    torch = _torch()
+    from paper_1708_02188_b200.virtual import VirtualRanks
+
+    monkeypatch.setenv("RBX_LL_ONESHOT_BYTES", oneshot_bytes)
+    g = golden("replay_digests")
+    for n, dims in all_dims():
+        vr = VirtualRanks(dims, nblocks_per_rank=2)
+        for dtype in ("i64", "f32", "f64"):
+            for it, length in enumerate(LENGTHS):
+                parts = [orc.generate_input(n, it, r, length, dtype) for r in range(n)]
+                out = run(vr, parts, "allreduce", "ll", None)
+                assert {orc.sha256(o) for o in out} == {g[f"{dkey(dims)}:{dtype}:{it}:{length}"]}, (dims, dtype, length)
+        vr.close()
+    del torch
+
+
+def test_ll_limits_and_large_ragged_inputs():
+    """MODE_LL (8-byte {data, epoch} words, no flags): every size up to its
+    1 MiB-per-rank cap is bit-exact, and a larger buffer is refused, not truncated."""
+    torch = _torch()
+    from paper_1708_02188_b200.virtual import VirtualRanks
+
+    for dims in [(2,), (2, 2, 2), (4, 2), (3,)]:
+        n = int(np.prod(dims))
+        grid = orc.Grid(dims)
+        vr = VirtualRanks(dims, nblocks_per_rank=8)
+        for length in (262_144, 262_143, 99_991):
+            parts = [orc.generate_input(6, 0, r, length, "f32") for r in range(n)]
+            want = orc.closed_form_allreduce(grid, parts)
+            ts = [torch.from_numpy(p.copy()).cuda() for p in parts]
+            vr.collective(ts, mode="ll")
+            torch.cuda.synchronize()
+            vr.check()
+            for t in ts:
+                assert np.array_equal(t.cpu().numpy(), want), (dims, length)
+        for length in (131_072, 65_537):
+            parts = [orc.generate_input(7, 0, r, length, "f64") for r in range(n)]
+            want = orc.closed_form_allreduce(grid, parts)
+            ts = [torch.from_numpy(p.copy()).cuda() for p in parts]
+            vr.collective(ts, mode="ll")
+            torch.cuda.synchronize()
+            for t in ts:
+                assert np.array_equal(t.cpu().numpy(), want), (dims, length)
+        too_big = [torch.zeros(262_145, device="cuda") for _ in range(n)]
+        with pytest.raises(ValueError):
+            vr.collective(too_big, mode="ll")
+        with pytest.raises(ValueError):
+            vr.collective([torch.zeros(100, device="cuda") for _ in range(n)], mode="ll", window=(0, 50))
+        vr.close()
 
 
 @pytest.mark.parametrize("mode", ["local", "fused", "push"])

@@ -59,17 +59,21 @@ def main():
             for v in views:
                 dist.all_reduce(v)
 
+    tiny = torch.zeros(1, device=dev)
     for variant in ("ours_bucket_list_one_launch", "ours_per_bucket", "nccl_per_bucket"):
         ts = []
         for it in range(args.iters + 2):
             flat.copy_(pristine)
             scratch.fill_(1.0)
             scratch.sum()
-            torch.cuda._sleep(100_000)
+            if it == 0:
+                dist.barrier()
+            # both arms: host ~0.5 ms ahead, then a device-side barrier of the arm's own kind
+            torch.cuda._sleep(1_000_000)
             if variant.startswith("ours"):
                 ctx.barrier()
             else:
-                dist.barrier()
+                dist.all_reduce(tiny)
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record(stream)
             run(variant)

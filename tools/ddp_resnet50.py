@@ -22,7 +22,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--comm", choices=["ours", "nccl"], default="ours")
+    ap.add_argument("--comm", choices=["ours", "nccl", "nccl_hook"], default="ours")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--batch", type=int, default=32)  # per GPU
@@ -60,6 +60,13 @@ def main():
             ctx = RankContext(rank, Grid(dims), group=gloo, device=local, nblocks=args.nblocks, blocking=False)
             hook_state = MultiringHookState(ctx)
             model.register_comm_hook(hook_state, multiring_allreduce_hook)
+        elif args.comm == "nccl_hook":  # the same Python-hook machinery around NCCL: isolates hook cost
+            def nccl_hook(_, bucket):
+                t = bucket.buffer()
+                fut = dist.all_reduce(t, async_op=True).get_future()
+                return fut.then(lambda f: f.value()[0].div_(world))
+
+            model.register_comm_hook(None, nccl_hook)
     opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9)
     x = torch.randn(args.batch, 3, 224, 224, device=dev).to(memory_format=torch.channels_last)
     y = torch.randint(0, 1000, (args.batch,), device=dev)

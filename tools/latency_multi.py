@@ -30,13 +30,15 @@ def main():
     dims = {2: (2,), 4: (2, 2), 8: (2, 2, 2)}[world]
     ctx = RankContext(rank, Grid(dims), device=rank, blocking=False)
     stream = torch.cuda.current_stream(dev)
-    for n in (1, 65536, 1048576, 25600000):
+    sizes = [int(x) for x in os.environ.get("LAT_SIZES", "1,65536,1048576,25600000").split(",")]
+    for n in sizes:
         work = ctx.empty(n, "f32")
         work.fill_(1.0)
-        for mode in ("fused", "ring_dims"):
+        modes = os.environ.get("LAT_MODES", "fused,ring_dims,ll").split(",")
+        for mode in [m for m in modes if m != "ll" or n * 4 <= (1 << 20)]:
             ts = []
             for it in range(12):
-                torch.cuda._sleep(100_000)  # host runs ahead of the device
+                torch.cuda._sleep(1_000_000)  # host runs ahead of the device
                 ctx.barrier()
                 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 s.record(stream)
@@ -51,9 +53,10 @@ def main():
             if rank == 0:
                 print(json.dumps({"n": n, "mode": mode, "event_us_median": round(t.median().item(), 2),
                                   "trace_rank0": tr}), flush=True)
-    # barrier alone
+    # barrier alone (host ahead: the spin before the start event hides Python launch cost)
     ts = []
     for it in range(12):
+        torch.cuda._sleep(1_000_000)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record(stream)
         ctx.barrier()
@@ -66,6 +69,7 @@ def main():
     ts = []
     x = torch.empty(1, device=dev)
     for it in range(12):
+        torch.cuda._sleep(1_000_000)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record(stream)
         x.fill_(0.0)

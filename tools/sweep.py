@@ -3,8 +3,10 @@ multi-ring kernel vs NCCL all_reduce, bus GB/s and % of 900 GB/s.
 
   torchrun --nproc-per-node N tools/sweep.py [--max-bytes 1073741824] [--out profiles/sweep_N.jsonl]
 
-Each point: inputs restored + L2 flushed outside the timed region, device flag
-barrier, CUDA events around one collective, max over ranks, median of --iters.
+Each point: inputs restored + L2 flushed outside the timed region, host ~0.5 ms
+ahead of the device, a device-side barrier of the arm's own kind (our flag
+barrier / a 1-element NCCL allreduce), CUDA events around one collective, max
+over ranks, trimmed mean (middle 80 %) of --iters.
 One JSON line per (dtype, bytes, impl) on rank 0.
 """
 
@@ -50,17 +52,22 @@ def main():
             work = ctx.empty(n, dt)
             pristine = torch.randn(n, device=dev).to(tdt[dt])
             res = {}
+            tiny = torch.zeros(1, device=dev)
             for impl in ("ours", "nccl"):
                 ts = []
                 for it in range(args.iters + 2):
                     work.copy_(pristine)
                     scratch.fill_(1.0)
                     scratch.sum()
-                    torch.cuda._sleep(100_000)  # host runs ahead: events time the kernel, not launch latency
+                    if it == 0:
+                        dist.barrier()
+                    # both arms: the host runs ~0.5 ms ahead (Python launch cost hidden), then a
+                    # device-side barrier of the arm's own kind aligns the GPUs before the start event
+                    torch.cuda._sleep(1_000_000)
                     if impl == "ours":
                         ctx.barrier()
                     else:
-                        dist.barrier()
+                        dist.all_reduce(tiny)
                     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     s.record(stream)
                     if impl == "ours":
@@ -73,7 +80,10 @@ def main():
                         ts.append(s.elapsed_time(e))
                 t = torch.tensor(ts, device=dev)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                sec = t.median().item() / 1e3
+                # events tick in ~2 us steps here: a trimmed mean (middle 80 %) resolves below that
+                srt = t.sort().values
+                k = len(srt) // 10
+                sec = srt[k:len(srt) - k].mean().item() / 1e3
                 bus = 2 * (world - 1) / world * nbytes / sec / 1e9
                 res[impl] = (sec, bus)
             ctx.check()
