@@ -122,6 +122,10 @@ struct rbx_comm {
   size_t bytes_per_cta = 32 * 1024;   // adaptive CTA count per call; env RBX_BYTES_PER_CTA
   int min_blocks = 16;                // env RBX_MIN_BLOCKS
   unsigned long long* trace_dev = nullptr;  // 64-word kernel timeline when RBX_TRACE is set
+  // specialised local kernel: CTAs per SM (0 = occupancy limit); env RBX_LOCAL_CTAS_PER_SM.
+  // 1 x 512 threads per SM measured 0.967-0.972 of the copy peak vs 0.925-0.928 at the
+  // occupancy limit (2 per SM) on config 2 (profiles/r01_local_ctas_per_sm.txt).
+  int local_ctas_per_sm = 1;
   bool local_specialised = true;  // MODE_LOCAL uses rbx_local_kernel where the shape has one; env RBX_LOCAL_GENERIC=1
   // MODE_PUSH inboxes: this rank's (registered, symmetric) and every rank's mapping
   char* inbox_local = nullptr;
@@ -265,6 +269,7 @@ int common_init(rbx_comm* c, const int* dims, int ndims, int device, int threads
   if (const char* t = std::getenv("RBX_TILE")) c->tile = std::atoi(t);
   if (const char* t = std::getenv("RBX_LOCAL_TILE")) c->local_tile = std::atoi(t);
   if (const char* t = std::getenv("RBX_LOCAL_GENERIC")) c->local_specialised = std::atoi(t) == 0;
+  if (const char* t = std::getenv("RBX_LOCAL_CTAS_PER_SM")) c->local_ctas_per_sm = std::atoi(t);
   if (const char* t = std::getenv("RBX_BYTES_PER_CTA")) c->bytes_per_cta = (size_t)std::max(1L, std::atol(t));
   if (const char* t = std::getenv("RBX_MIN_BLOCKS")) c->min_blocks = std::max(1, std::atoi(t));
   if (const char* t = std::getenv("RBX_LL_AUTO_BYTES"))
@@ -515,14 +520,18 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
   for (int k = 0; k < nbufs; ++k) total += counts[k];
   if (total == 0 && op != RBX_OP_BARRIER) return RBX_OK;  // empty collective: nothing moves on any rank
   const bool whole = lo == 0 && (hi < 0 || hi == (int64_t)total);
-  if (mode == RBX_MODE_LL) {
+  const bool ll = mode == RBX_MODE_LL || (mode == RBX_MODE_AUTO && op == RBX_OP_ALLREDUCE && nbufs == 1 && whole &&
+                                          c->nranks > 1 && total * (size_t)es <= c->ll_auto_bytes);
+  if (ll) {
     if (op != RBX_OP_ALLREDUCE || nbufs != 1 || !whole)
       return fail(RBX_ERR_INVALID, "MODE_LL supports a whole-buffer single allreduce only");
+    // LL never maps the buffer into peers, but the contract is the same for every
+    // mode: collectives run on registered (symmetric) buffers only
+    int id;
+    size_t off;
+    if (int rc = find_buffer(c, bufs[0], counts[0] * es, &id, &off)) return rc;
     return ll_launch(c, {c->rank}, bufs, counts[0], dtype, stream, false);
   }
-  if (mode == RBX_MODE_AUTO && op == RBX_OP_ALLREDUCE && nbufs == 1 && whole && c->nranks > 1 &&
-      total * (size_t)es <= c->ll_auto_bytes)
-    return ll_launch(c, {c->rank}, bufs, counts[0], dtype, stream, false);
   std::vector<const void*> kp(bufs, bufs + nbufs);
   std::vector<size_t> kc(counts, counts + nbufs);
   const std::string key = plan_key(op, mode, dtype, kp, kc) + "@" + std::to_string(lo) + ":" + std::to_string(hi);
@@ -1065,6 +1074,7 @@ int rbx_vcollective_window(rbx_comm_t* c, void* const* bufs, size_t count, size_
         RBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, c->threads, 0));
         cp.local_fn = fn;
         cp.local_args = args;
+        if (c->local_ctas_per_sm > 0) per_sm = std::min(per_sm, c->local_ctas_per_sm);
         cp.local_grid = std::max(1, per_sm) * c->sm_count;
       }
     }

@@ -86,26 +86,69 @@ __device__ __forceinline__ unsigned long long ld_ll(const unsigned long long* p)
   return v;
 }
 
-// word w of element range starting at element `o` of a buffer of T
+// LL word format of a dtype.  A fold UNIT is what one thread folds at once:
+// 2-byte types pack two elements per 32-bit payload (unit = 1 word, 2 lanes),
+// 4-byte types one element per word, 8-byte types one element in two words.
+// Words of a region are numbered from the region's first element; a region of
+// `len` elements has nunits(len) * WPU words, never more than len * WPU, so
+// element-offset based slot addressing (one-shot) cannot overlap.
 template <typename T>
-__device__ __forceinline__ uint32_t ll_load_word(const char* buf, int64_t o, int64_t w) {
-  if (sizeof(T) == 2) return (uint32_t)__ldcg(reinterpret_cast<const unsigned short*>(buf) + o + w);
-  return __ldcg(reinterpret_cast<const unsigned int*>(buf + o * (int64_t)sizeof(T)) + w);
-}
-template <typename T>
-__device__ __forceinline__ void ll_store_word(char* buf, int64_t o, int64_t w, uint32_t v) {
-  if (sizeof(T) == 2)
-    reinterpret_cast<unsigned short*>(buf)[o + w] = (unsigned short)v;
-  else
-    reinterpret_cast<unsigned int*>(buf + o * (int64_t)sizeof(T))[w] = v;
-}
+struct LLFmt {
+  static constexpr int ES = sizeof(T);
+  static constexpr int WPU = ES == 8 ? 2 : 1;  // words per unit
+  static constexpr int LPU = ES == 2 ? 2 : 1;  // lanes (elements) per unit
+  using Acc = typename Traits<T>::Acc;
+  __device__ static int64_t nunits(int64_t len) { return ES == 2 ? (len + 1) / 2 : len; }
+  __device__ static int64_t nwords(int64_t len) { return nunits(len) * WPU; }
+  // payload of word w of the region [o, o+len) of buf
+  __device__ static uint32_t load(const char* buf, int64_t o, int64_t len, int64_t w) {
+    if (ES == 2) {
+      const unsigned short* p = reinterpret_cast<const unsigned short*>(buf) + o + 2 * w;
+      const uint32_t lo = __ldcg(p);
+      const uint32_t hi = 2 * w + 1 < len ? (uint32_t)__ldcg(p + 1) : 0u;
+      return lo | (hi << 16);
+    }
+    return __ldcg(reinterpret_cast<const unsigned int*>(buf + o * (int64_t)ES) + w);
+  }
+  __device__ static void store(char* buf, int64_t o, int64_t len, int64_t w, uint32_t v) {
+    if (ES == 2) {
+      unsigned short* p = reinterpret_cast<unsigned short*>(buf) + o + 2 * w;
+      p[0] = (unsigned short)v;
+      if (2 * w + 1 < len) p[1] = (unsigned short)(v >> 16);
+      return;
+    }
+    reinterpret_cast<unsigned int*>(buf + o * (int64_t)ES)[w] = v;
+  }
+  __device__ static void lanes(const uint32_t (&w)[WPU], Acc (&x)[LPU]) {
+    using B = typename Traits<T>::Bits;
+    if (ES == 2) {
+      x[0] = Traits<T>::from_bits((B)(w[0] & 0xffffu));
+      x[LPU - 1] = Traits<T>::from_bits((B)(w[0] >> 16));
+    } else if (ES == 8) {
+      x[0] = Traits<T>::from_bits((B)(((unsigned long long)w[WPU - 1] << 32) | w[0]));
+    } else {
+      x[0] = Traits<T>::from_bits((B)w[0]);
+    }
+  }
+  __device__ static void pack(const Acc (&x)[LPU], uint32_t (&w)[WPU]) {
+    if (ES == 2) {
+      w[0] = (uint32_t)Traits<T>::to_bits(x[0]) | ((uint32_t)Traits<T>::to_bits(x[LPU - 1]) << 16);
+    } else if (ES == 8) {
+      const unsigned long long b = (unsigned long long)Traits<T>::to_bits(x[0]);
+      w[0] = (uint32_t)b;
+      w[WPU - 1] = (uint32_t)(b >> 32);
+    } else {
+      w[0] = (uint32_t)Traits<T>::to_bits(x[0]);
+    }
+  }
+};
 
 struct LLWait {
   uint32_t e;
   uint64_t t0, timeout_ns;
   volatile uint32_t* abort_word;
   bool failed;
-  // payload of the word at p once its epoch is current; false on timeout/abort
+  // payload of the word at p once its epoch is current (0 on timeout/abort, failed set)
   __device__ __forceinline__ uint32_t get(const unsigned long long* p) {
     uint32_t it = 0;
     while (true) {
@@ -122,18 +165,59 @@ struct LLWait {
   }
 };
 
-template <typename T>
-__device__ __forceinline__ typename Traits<T>::Acc ll_value(uint32_t lo, uint32_t hi) {
-  using B = typename Traits<T>::Bits;
-  if (sizeof(T) == 8) return Traits<T>::from_bits((B)(((unsigned long long)hi << 32) | lo));
-  return Traits<T>::from_bits((B)lo);
+// Fold unit u of the region [o, o+len) from N sources in `order` (my own words
+// straight from buf, the others from LL slots: slot(p) + word index), then
+// return the packed result words.
+template <typename T, typename SlotFn>
+__device__ __forceinline__ void ll_fold_unit(const LLRank& R, const uint8_t* order, int N, int nlev, int64_t o,
+                                             int64_t len, int64_t u, SlotFn slot, LLWait& wt,
+                                             uint32_t (&res)[LLFmt<T>::WPU]) {
+  using F = LLFmt<T>;
+  using Acc = typename Traits<T>::Acc;
+  constexpr int WPU = F::WPU, LPU = F::LPU;
+  const uint32_t e = wt.e;
+  // issue every source's word(s) at once, then re-poll the ones not yet current
+  unsigned long long raw[RBX_MAX_RANKS][WPU];
+#pragma unroll
+  for (int k = 0; k < RBX_MAX_RANKS; ++k) {
+    if (k < N) {
+      const int p = order[k];
+#pragma unroll
+      for (int j = 0; j < WPU; ++j)
+        raw[k][j] = p == R.me ? (((unsigned long long)e << 32) | F::load(R.buf, o, len, u * WPU + j))
+                              : ld_ll(slot(p) + u * WPU + j);
+    }
+  }
+  FoldState<T, LPU, RBX_MAX_LEVELS> f;
+#pragma unroll
+  for (int k = 0; k < RBX_MAX_RANKS; ++k) {
+    if (k < N) {
+      const int p = order[k];
+      uint32_t w[WPU];
+#pragma unroll
+      for (int j = 0; j < WPU; ++j)
+        w[j] = (uint32_t)(raw[k][j] >> 32) == e ? (uint32_t)raw[k][j] : wt.get(slot(p) + u * WPU + j);
+      Acc x[LPU];
+      F::lanes(w, x);
+      f.feed(R.ctrl[k], x);
+    }
+  }
+  Acc r[LPU];
+#pragma unroll
+  for (int l = 0; l < LPU; ++l) {
+    r[l] = f.a[0][l];
+#pragma unroll
+    for (int L = 1; L < RBX_MAX_LEVELS; ++L)
+      if (L == nlev - 1) r[l] = f.a[L][l];
+  }
+  F::pack(r, res);
 }
 
 template <typename T>
-__global__ void __launch_bounds__(512) rbx_ll_kernel(const __grid_constant__ LLArgs a) {
-  using Acc = typename Traits<T>::Acc;
-  constexpr int W = sizeof(T) == 8 ? 2 : 1;  // LL words per element
-  constexpr int U = 4;                       // words per thread in flight (phases 1 and 3)
+__global__ void __launch_bounds__(512, 1) rbx_ll_kernel(const __grid_constant__ LLArgs a) {
+  using F = LLFmt<T>;
+  constexpr int WPU = F::WPU;
+  constexpr int U = 4;  // words per thread in flight (scatter / gather)
   const int v = blockIdx.x / a.nb, b = blockIdx.x % a.nb;
   const LLRank& R = a.rank[v];
   const int N = a.nranks, me = R.me;
@@ -160,162 +244,98 @@ __global__ void __launch_bounds__(512) rbx_ll_kernel(const __grid_constant__ LLA
   unsigned long long* own = R.area[me];
 
   if (a.oneshot) {
-    // my whole buffer -> every peer's slot [parity][me]; then fold every element.
-    // The same thread pushes and folds element i (it overwrites buf[i] last).
+    // my whole buffer -> every peer's slot [parity][me]; then fold every unit.
+    // The same thread pushes and folds unit u of region q (it overwrites it last).
     const int64_t par = (int64_t)(e & 1u) * N * ll_cap1_words();
     for (int q = 0; q < N; ++q) {
-      const int64_t o = R.off[q], n = R.len[q];
-      for (int64_t i = tid; i < n; i += nthr) {
-        uint32_t mine[W];
+      const int64_t o = R.off[q], len = R.len[q], nu = F::nunits(len);
+      for (int64_t u = tid; u < nu; u += nthr) {
 #pragma unroll
-        for (int j = 0; j < W; ++j) mine[j] = ll_load_word<T>(R.buf, o, i * W + j);
-        for (int k = 1; k < N; ++k) {
-          unsigned long long* dst = R.area[(me + k) % N] + ll_oneshot_off(N) + par + (int64_t)me * ll_cap1_words() +
-                                    (o + i) * W;
-#pragma unroll
-          for (int j = 0; j < W; ++j) st_ll(dst + j, mine[j], e);
+        for (int j = 0; j < WPU; ++j) {
+          const uint32_t d = F::load(R.buf, o, len, u * WPU + j);
+          for (int k = 1; k < N; ++k)
+            st_ll(R.area[(me + k) % N] + ll_oneshot_off(N) + par + (int64_t)me * ll_cap1_words() + o * WPU + u * WPU + j,
+                  d, e);
         }
       }
     }
     if (tr) tr[3] = global_ns();
     const unsigned long long* slots = own + ll_oneshot_off(N) + par;
     for (int q = 0; q < N; ++q) {
-      const int64_t o = R.off[q], n = R.len[q];
-      for (int64_t i = tid; i < n; i += nthr) {
-        unsigned long long raw[RBX_MAX_RANKS][W];
-#pragma unroll
-        for (int k = 0; k < RBX_MAX_RANKS; ++k) {
-          if (k < N) {
-            const int p = a.orders.of[q][k];
-#pragma unroll
-            for (int j = 0; j < W; ++j)
-              raw[k][j] = p == me ? (((unsigned long long)e << 32) | ll_load_word<T>(R.buf, o, i * W + j))
-                                  : ld_ll(slots + (int64_t)p * ll_cap1_words() + (o + i) * W + j);
-          }
-        }
-        FoldState<T, 1, RBX_MAX_LEVELS> f;
-#pragma unroll
-        for (int k = 0; k < RBX_MAX_RANKS; ++k) {
-          if (k < N) {
-            const int p = a.orders.of[q][k];
-            uint32_t x2[W];
-#pragma unroll
-            for (int j = 0; j < W; ++j)
-              x2[j] = (uint32_t)(raw[k][j] >> 32) == e
-                          ? (uint32_t)raw[k][j]
-                          : wt.get(slots + (int64_t)p * ll_cap1_words() + (o + i) * W + j);
-            const Acc x[1] = {ll_value<T>(x2[0], x2[W - 1])};
-            f.feed(R.ctrl[k], x);
-          }
-        }
-        Acc r = f.a[0][0];
-#pragma unroll
-        for (int L = 1; L < RBX_MAX_LEVELS; ++L)
-          if (L == a.nlev - 1) r = f.a[L][0];
-        const unsigned long long bits = (unsigned long long)Traits<T>::to_bits(r);
-        const uint32_t rw[2] = {(uint32_t)bits, (uint32_t)(bits >> 32)};
+      const int64_t o = R.off[q], len = R.len[q], nu = F::nunits(len);
+      auto slot = [&](int p) { return slots + (int64_t)p * ll_cap1_words() + o * WPU; };
+      for (int64_t u = tid; u < nu; u += nthr) {
+        uint32_t res[WPU];
+        ll_fold_unit<T>(R, a.orders.of[q], N, a.nlev, o, len, u, slot, wt, res);
         if (!wt.failed) {
 #pragma unroll
-          for (int j = 0; j < W; ++j) ll_store_word<T>(R.buf, o, i * W + j, rw[j]);
+          for (int j = 0; j < WPU; ++j) F::store(R.buf, o, len, u * WPU + j, res[j]);
         }
       }
     }
     if (tr) tr[4] = tr[5] = global_ns();
   } else {
-  // 1. scatter my input of every peer's region into that peer's slot [me]
-  for (int k = 1; k < N; ++k) {
-    const int q = (me + k) % N;
-    const int64_t o = R.off[q], nw = R.len[q] * W;
-    unsigned long long* dst = R.area[q] + (int64_t)me * cap;
-    for (int64_t w0 = tid; w0 < nw; w0 += nthr * U) {
-      uint32_t d[U];
+    // 1. scatter my input of every peer's region into that peer's slot [me]
+    for (int k = 1; k < N; ++k) {
+      const int q = (me + k) % N;
+      const int64_t o = R.off[q], len = R.len[q], nw = F::nwords(len);
+      unsigned long long* dst = R.area[q] + (int64_t)me * cap;
+      for (int64_t w0 = tid; w0 < nw; w0 += nthr * U) {
+        uint32_t d[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t w = w0 + u * nthr;
-        d[u] = w < nw ? ll_load_word<T>(R.buf, o, w) : 0u;
-      }
+        for (int u = 0; u < U; ++u) {
+          const int64_t w = w0 + u * nthr;
+          d[u] = w < nw ? F::load(R.buf, o, len, w) : 0u;
+        }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t w = w0 + u * nthr;
-        if (w < nw) st_ll(dst + w, d[u], e);
+        for (int u = 0; u < U; ++u) {
+          const int64_t w = w0 + u * nthr;
+          if (w < nw) st_ll(dst + w, d[u], e);
+        }
       }
     }
-  }
-
-  if (tr) tr[3] = global_ns();
-  // 2. fold my region in the reference order; result -> my buffer + every peer's gather slot [me]
-  {
-    const int64_t o = R.off[me], n = R.len[me];
-    for (int64_t i = tid; i < n; i += nthr) {
-      // issue every source's word(s) at once, then re-poll the ones not yet current
-      unsigned long long raw[RBX_MAX_RANKS][W];
+    if (tr) tr[3] = global_ns();
+    // 2. fold my region in the reference order; result -> my buffer + every peer's gather slot [me]
+    {
+      const int64_t o = R.off[me], len = R.len[me], nu = F::nunits(len);
+      auto slot = [&](int p) { return (const unsigned long long*)(own + (int64_t)p * cap); };
+      for (int64_t u = tid; u < nu; u += nthr) {
+        uint32_t res[WPU];
+        ll_fold_unit<T>(R, R.order, N, a.nlev, o, len, u, slot, wt, res);
 #pragma unroll
-      for (int k = 0; k < RBX_MAX_RANKS; ++k) {
-        if (k < N) {
-          const int p = R.order[k];
+        for (int j = 0; j < WPU; ++j) F::store(R.buf, o, len, u * WPU + j, res[j]);
+        for (int k = 1; k < N; ++k) {
+          unsigned long long* dst = R.area[(me + k) % N] + (int64_t)(N + me) * cap + u * WPU;
 #pragma unroll
-          for (int j = 0; j < W; ++j) {
-            raw[k][j] = p == me ? (((unsigned long long)e << 32) | ll_load_word<T>(R.buf, o, i * W + j))
-                                : ld_ll(own + (int64_t)p * cap + i * W + j);
+          for (int j = 0; j < WPU; ++j) st_ll(dst + j, res[j], e);
+        }
+      }
+    }
+    if (tr) tr[4] = global_ns();
+    // 3. gather every peer's result from my gather slots
+    for (int k = 1; k < N; ++k) {
+      const int q = (me + k) % N;
+      const int64_t o = R.off[q], len = R.len[q], nw = F::nwords(len);
+      const unsigned long long* src = own + (int64_t)(N + q) * cap;
+      for (int64_t w0 = tid; w0 < nw; w0 += nthr * U) {
+        unsigned long long raw[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t w = w0 + u * nthr;
+          raw[u] = w < nw ? ld_ll(src + w) : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t w = w0 + u * nthr;
+          if (w < nw) {
+            const uint32_t d = (uint32_t)(raw[u] >> 32) == e ? (uint32_t)raw[u] : wt.get(src + w);
+            if (!wt.failed) F::store(R.buf, o, len, w, d);
           }
         }
       }
-      FoldState<T, 1, RBX_MAX_LEVELS> f;
-#pragma unroll
-      for (int k = 0; k < RBX_MAX_RANKS; ++k) {
-        if (k < N) {
-          const int p = R.order[k];
-          uint32_t x2[W];
-#pragma unroll
-          for (int j = 0; j < W; ++j)
-            x2[j] = (uint32_t)(raw[k][j] >> 32) == e ? (uint32_t)raw[k][j]
-                                                      : wt.get(own + (int64_t)p * cap + i * W + j);
-          const Acc x[1] = {ll_value<T>(x2[0], x2[W - 1])};
-          f.feed(R.ctrl[k], x);
-        }
-      }
-      Acc r = f.a[0][0];
-#pragma unroll
-      for (int L = 1; L < RBX_MAX_LEVELS; ++L)
-        if (L == a.nlev - 1) r = f.a[L][0];
-      const unsigned long long bits = (unsigned long long)Traits<T>::to_bits(r);
-      const uint32_t rw[2] = {(uint32_t)bits, (uint32_t)(bits >> 32)};
-#pragma unroll
-      for (int j = 0; j < W; ++j) ll_store_word<T>(R.buf, o, i * W + j, rw[j]);
-      for (int k = 1; k < N; ++k) {
-        unsigned long long* dst = R.area[(me + k) % N] + (int64_t)(N + me) * cap + i * W;
-#pragma unroll
-        for (int j = 0; j < W; ++j) st_ll(dst + j, rw[j], e);
-      }
     }
+    if (tr) tr[5] = global_ns();
   }
-
-  if (tr) tr[4] = global_ns();
-  // 3. gather every peer's result from my gather slots
-  for (int k = 1; k < N; ++k) {
-    const int q = (me + k) % N;
-    const int64_t o = R.off[q], nw = R.len[q] * W;
-    const unsigned long long* src = own + (int64_t)(N + q) * cap;
-    for (int64_t w0 = tid; w0 < nw; w0 += nthr * U) {
-      unsigned long long raw[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t w = w0 + u * nthr;
-        raw[u] = w < nw ? ld_ll(src + w) : 0ull;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t w = w0 + u * nthr;
-        if (w < nw) {
-          const uint32_t d = (uint32_t)(raw[u] >> 32) == e ? (uint32_t)raw[u] : wt.get(src + w);
-          if (!wt.failed) ll_store_word<T>(R.buf, o, w, d);
-        }
-      }
-    }
-  }
-
-  if (tr) tr[5] = global_ns();
-  }  // two-shot
 
   if (tr) tr[30] = global_ns();
   if (wt.failed) s_fail = 1;

@@ -221,6 +221,15 @@ def test_ll_limits_and_large_ragged_inputs():
             torch.cuda.synchronize()
             for t in ts:
                 assert np.array_equal(t.cpu().numpy(), want), (dims, length)
+        for length in (524_288, 524_287, 77_777):  # bf16: two elements per LL word, odd regions
+            rng = np.random.default_rng(length)
+            bits = [orc.bf16_round(rng.standard_normal(length).astype(np.float32)) for _ in range(n)]
+            want = orc.bf16_allreduce(grid, bits)
+            ts = [torch.from_numpy(b.view(np.int16)).cuda().view(torch.bfloat16) for b in bits]
+            vr.collective(ts, mode="ll")
+            torch.cuda.synchronize()
+            for t in ts:
+                assert np.array_equal(t.view(torch.int16).cpu().numpy().view(np.uint16), want), (dims, length)
         too_big = [torch.zeros(262_145, device="cuda") for _ in range(n)]
         with pytest.raises(ValueError):
             vr.collective(too_big, mode="ll")
@@ -229,7 +238,7 @@ def test_ll_limits_and_large_ragged_inputs():
         vr.close()
 
 
-@pytest.mark.parametrize("mode", ["local", "fused", "push"])
+@pytest.mark.parametrize("mode", ["local", "fused", "push", "ll"])
 def test_cuda_graph_replay(mode):
     """Epochs live in device memory, so a captured launch replays correctly
     (CUDA graphs instead of per-call launches for static buffers)."""
