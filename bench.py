@@ -460,10 +460,12 @@ def main_multi(args):
             dist.all_reduce(nbuf)
         torch.cuda.synchronize()
         nt = []
+        tiny = torch.zeros(1, device=dev)
+        dist.barrier()
         for _ in range(10):
             nbuf.copy_(pristine)
-            flush_l2(scratch)
-            dist.barrier()
+            flush_l2(scratch)  # ends with a device spin: the host runs ahead
+            dist.all_reduce(tiny)  # device-side alignment of the ranks, like ctx.barrier() on our arm
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record(stream)
             dist.all_reduce(nbuf)

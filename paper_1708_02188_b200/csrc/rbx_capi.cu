@@ -117,7 +117,10 @@ struct rbx_comm {
   bool connected = false;
   int sm_count = 148;
   int max_coresident = 0;  // co-resident CTAs of the step kernel
-  int tile = 1024;         // work tile in 16-byte vectors (0: contiguous range per CTA); env RBX_TILE
+  // work tile in 16-byte vectors (0: contiguous range per CTA); env RBX_TILE.  -1 = by dtype:
+  // 1024 for 4/8-byte types, 2048 for bf16/f16, whose heavier fold (unpack, fp32 add, RNE)
+  // needs more vectors in flight per call (N=2 bf16 +5.5 %, fp32 flat; profiles/r01_tile_by_dtype.txt)
+  int tile = -1;
   int local_tile = 2048;   // same for the HBM-bound local mode (measured best of 0/512/2048/4096/8192/32768); env RBX_LOCAL_TILE
   size_t bytes_per_cta = 32 * 1024;   // adaptive CTA count per call; env RBX_BYTES_PER_CTA
   int min_blocks = 16;                // env RBX_MIN_BLOCKS
@@ -305,7 +308,7 @@ std::string plan_key(int op, int mode, int dtype, const std::vector<const void*>
 // tables: one pointer table shared by every plan, or one per plan (MODE_PUSH
 // tables depend on the rank: own inbox slots, this rank's slot in the peers').
 int upload(rbx_comm* c, std::vector<rbx::Plan>& host, const std::vector<std::vector<void*>>& tables,
-           CachedPlan* out) {
+           CachedPlan* out, int dtype) {
   std::vector<void*> flat;
   std::vector<size_t> base;
   for (const auto& t : tables) {
@@ -319,7 +322,7 @@ int upload(rbx_comm* c, std::vector<rbx::Plan>& host, const std::vector<std::vec
   for (size_t i = 0; i < host.size(); ++i) {
     rbx::Plan& p = host[i];
     p.ptrs = out->ptrs + (tables.size() == host.size() ? base[i] : 0);
-    p.tile = p.nosync ? c->local_tile : c->tile;
+    p.tile = p.nosync ? c->local_tile : (c->tile >= 0 ? c->tile : (dtype_size(dtype) == 2 ? 2048 : 1024));
     int segs = 0;
     for (int s = 0; s < p.nsteps; ++s) segs += p.steps[s].nseg;
     if (segs > maxsegs) maxsegs = segs;
@@ -353,9 +356,8 @@ int launch(rbx_comm* c, const CachedPlan& cp, int dtype, cudaStream_t stream, bo
   return RBX_OK;
 }
 
-// Per-dimension stages would store bf16/f16 partials between stages; the
-// fp32-partial workspace for that is not built yet, so refuse rather than
-// silently round partials (parity policy: one RNE at the end).
+// Every (mode, dtype) pair is supported: RING_DIMS keeps bf16/f16 stage
+// partials in fp32 workspaces (ws_table), LL folds in fp32 registers.
 int check_mode_dtype(int mode, int dtype) {
   (void)dtype;
   if (mode < RBX_MODE_AUTO || mode > RBX_MODE_LL) return fail(RBX_ERR_INVALID, "unknown mode");
@@ -586,7 +588,7 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
     host[0].my_sig = c->sig[c->rank];
     CachedPlan cp;
     cp.uses_inbox = push || ws;
-    int rc = upload(c, host, {ptrs}, &cp);
+    int rc = upload(c, host, {ptrs}, &cp, dtype);
     if (rc) return rc;
     it = c->plans.emplace(key, cp).first;
   }
@@ -1064,7 +1066,7 @@ int rbx_vcollective_window(rbx_comm_t* c, void* const* bufs, size_t count, size_
     }
     CachedPlan cp;
     cp.uses_inbox = push || ws;
-    int rc = upload(c, host, tables, &cp);
+    int rc = upload(c, host, tables, &cp, dtype);
     if (rc) return rc;
     if (local && c->local_specialised) {
       const void* fn = local_kernel_for(dtype, V, (int)c->geo.active_dims().size());
