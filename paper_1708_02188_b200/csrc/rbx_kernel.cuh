@@ -21,6 +21,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "rbx_plan.h"
 
 namespace rbx {
@@ -198,6 +200,32 @@ struct FoldState {
   __device__ __forceinline__ Acc result(int l) const { return a[NLEV - 1][l]; }
 };
 
+// 16 bytes of results from the accumulators of one vector.  16-bit types
+// narrow lane pairs with one cvt.rn.{bf16x2,f16x2}.f32 each: the same RNE as
+// the per-lane narrow, with half the conversions and no bit inserts.
+template <typename T, int LANES, int NLEV>
+__device__ __forceinline__ int4 pack_result(const FoldState<T, LANES, NLEV>& st) {
+  int4 packed = make_int4(0, 0, 0, 0);
+  if constexpr (sizeof(T) == 2 && LANES % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < LANES / 2; ++i) {
+      uint32_t w;
+      if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+        const __nv_bfloat162 h = __floats2bfloat162_rn(st.result(2 * i), st.result(2 * i + 1));
+        w = *reinterpret_cast<const uint32_t*>(&h);
+      } else {
+        const __half2 h = __floats2half2_rn(st.result(2 * i), st.result(2 * i + 1));
+        w = *reinterpret_cast<const uint32_t*>(&h);
+      }
+      set_word(packed, i, w);
+    }
+  } else {
+#pragma unroll
+    for (int l = 0; l < LANES; ++l) Traits<T>::put(packed, l, st.result(l));
+  }
+  return packed;
+}
+
 struct SegCtx {
   const char* src[RBX_MAX_RANKS];
   char* dst[RBX_MAX_RANKS];
@@ -271,9 +299,7 @@ __device__ __noinline__ void fold_body(const SegCtx& sc, int64_t body_off, int64
     for (int u = 0; u < U; ++u) {
       const int64_t idx = v + (int64_t)u * blockDim.x;
       if (idx < v1) {
-        int4 packed = make_int4(0, 0, 0, 0);
-#pragma unroll
-        for (int l = 0; l < VEC; ++l) Traits<T>::put(packed, l, st[u].result(l));
+        const int4 packed = pack_result(st[u]);
         for (int d = 0; d < sc.ndst; ++d) __stcg(reinterpret_cast<int4*>(sc.dst[d] + base + idx * 16), packed);
       }
     }
@@ -351,9 +377,7 @@ __device__ __noinline__ void fold_body_acc(const SegCtx& sc, int64_t body_off, i
           __stcg(reinterpret_cast<int4*>(sc.dst[d] + e * 4 + 16), hi);
         }
       } else {
-        int4 packed = make_int4(0, 0, 0, 0);
-#pragma unroll
-        for (int l = 0; l < VEC; ++l) Traits<T>::put(packed, l, st.result(l));
+        const int4 packed = pack_result(st);
         for (int d = 0; d < sc.ndst; ++d)
           __stcg(reinterpret_cast<int4*>(sc.dst[d] + e * (int64_t)sizeof(T)), packed);
       }

@@ -50,9 +50,7 @@ __global__ void __launch_bounds__(512) rbx_local_kernel(const __grid_constant__ 
       for (int l = 0; l < VEC; ++l) x[l] = Traits<T>::lane(raw[j], l);
       st.feed(sg.ctrl[j], x);
     }
-    int4 packed = make_int4(0, 0, 0, 0);
-#pragma unroll
-    for (int l = 0; l < VEC; ++l) Traits<T>::put(packed, l, st.result(l));
+    const int4 packed = pack_result(st);
 #pragma unroll
     for (int d = 0; d < V; ++d) __stcg(reinterpret_cast<int4*>(a.dst[d] + byte), packed);
   }
