@@ -268,6 +268,7 @@ int common_init(rbx_comm* c, const int* dims, int ndims, int device, int threads
   if (threads <= 0) threads = 512;
   if (threads % 32 || threads > 512) return fail(RBX_ERR_INVALID, "threads must be a multiple of 32 and <= 512");
   c->threads = threads;
+  c->ll_threads = threads;
   c->device = device;
   if (const char* t = std::getenv("RBX_TILE")) c->tile = std::atoi(t);
   if (const char* t = std::getenv("RBX_LOCAL_TILE")) c->local_tile = std::atoi(t);

@@ -22,13 +22,14 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--comm", choices=["ours", "nccl", "nccl_hook"], default="ours")
+    ap.add_argument("--comm", choices=["ours", "nccl", "nccl_hook", "noop_hook"], default="ours")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--batch", type=int, default=32)  # per GPU
     ap.add_argument("--amp", default="bf16", choices=["bf16", "none"])
     ap.add_argument("--nblocks", type=int, default=32, help="CTAs of the allreduce kernel (leave SMs to backward)")
     ap.add_argument("--bucket-view", type=int, default=1, help="gradient_as_bucket_view")
+    ap.add_argument("--threads", type=int, default=512, help="threads per CTA of the allreduce kernels")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -57,7 +58,8 @@ def main():
 
             dims = {2: (2,), 4: (2, 2), 8: (2, 2, 2)}.get(world, (world,))
             gloo = dist.new_group(backend="gloo")  # host plumbing for handle exchange
-            ctx = RankContext(rank, Grid(dims), group=gloo, device=local, nblocks=args.nblocks, blocking=False)
+            ctx = RankContext(rank, Grid(dims), group=gloo, device=local, nblocks=args.nblocks,
+                              threads=args.threads, blocking=False)
             hook_state = MultiringHookState(ctx)
             model.register_comm_hook(hook_state, multiring_allreduce_hook)
         elif args.comm == "nccl_hook":  # the same Python-hook machinery around NCCL: isolates hook cost
@@ -67,6 +69,13 @@ def main():
                 return fut.then(lambda f: f.value()[0].div_(world))
 
             model.register_comm_hook(None, nccl_hook)
+        elif args.comm == "noop_hook":  # hook machinery only, no communication at all (cost floor of any hook)
+            def noop_hook(_, bucket):
+                fut = torch.futures.Future(devices=[dev])
+                fut.set_result(bucket.buffer())
+                return fut
+
+            model.register_comm_hook(None, noop_hook)
     opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9)
     x = torch.randn(args.batch, 3, 224, 224, device=dev).to(memory_format=torch.channels_last)
     y = torch.randint(0, 1000, (args.batch,), device=dev)
@@ -102,7 +111,8 @@ def main():
         print(json.dumps({
             "config": "config5: ResNet-50 DDP step, synthetic 3x224x224, 1000 classes",
             "comm": args.comm if world > 1 else "none", "n_gpus": world, "batch_per_gpu": args.batch,
-            "nblocks": args.nblocks if args.comm == "ours" else None, "bucket_view": bool(args.bucket_view),
+            "nblocks": args.nblocks if args.comm == "ours" else None,
+            "threads": args.threads if args.comm == "ours" else None, "bucket_view": bool(args.bucket_view),
             "amp": args.amp, "params": nparams, "grad_bytes": nparams * 4,
             "t_iter_ms": round(t_ms, 3), "images_per_s": round(world * args.batch / t_ms * 1e3, 1),
             "loss": float(loss.item()),
