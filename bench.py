@@ -168,6 +168,25 @@ def pipelined_e2e(n, chunks, h2d, red, d2h, stream, iters, warmup, before):
     return out
 
 
+def bind_host_to_gpu(index: int) -> list:
+    """Pin this process to the CPU cores NVML reports as local to GPU `index`
+    (its PCIe root's NUMA node), so pinned host buffers for the e2e leg are
+    allocated and copied near the GPU.  Returns the cores, or [] if unknown."""
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cores = [w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1]
+        cores = [c for c in cores if c < os.cpu_count()]
+        if cores:
+            os.sched_setaffinity(0, cores)
+        return cores
+    except Exception:  # noqa: BLE001 -- best effort (no NVML / no permission)
+        return []
+
+
 def flush_l2(scratch):
     """Evict L2: write a 256 MiB buffer (> 126 MB L2), then read it back so the
     dirty lines are written back before the timed region starts (otherwise
@@ -249,7 +268,7 @@ def main_single(args):
     """N = 1: the 8 ranks of config 2 on one GPU, local-reduce kernel."""
     import torch
 
-    from oracle import ringbox_oracle as orc
+    from paper_1708_02188_b200.runtime import Workload, generate_input
     from paper_1708_02188_b200.virtual import VirtualRanks
 
     dims = tuple(int(x) for x in args.dims.split("x")) if args.dims else DIMS_FOR[1]
@@ -259,9 +278,11 @@ def main_single(args):
     n = args.elems
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
+    bind_host_to_gpu(0)
     tdt = torch.float32 if args.dtype == "f32" else torch.bfloat16
     esz = 4 if args.dtype == "f32" else 2
-    host = [torch.from_numpy(orc.generate_input(0, 0, r, n, "f32")).to(tdt) for r in range(ranks)]
+    wl = Workload(lengths=(n,), dtype="f32", seed=0)  # the reference's inputs (runtime.py:94-100)
+    host = [torch.from_numpy(generate_input(wl, 0, r, n)).to(tdt) for r in range(ranks)]
     pristine = [h.to(dev) for h in host]
     work = [torch.empty_like(p) for p in pristine]
     scratch = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > L2 (126 MB)
@@ -372,14 +393,14 @@ def main_multi(args):
     import torch
     import torch.distributed as dist
 
-    from oracle import ringbox_oracle as orc
     from paper_1708_02188_b200.multiring import Grid
-    from paper_1708_02188_b200.runtime import RankContext
+    from paper_1708_02188_b200.runtime import RankContext, Workload, generate_input
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    bind_host_to_gpu(local)
     dist.init_process_group("nccl", device_id=dev)
     dims = tuple(int(x) for x in args.dims.split("x")) if args.dims else DIMS_FOR.get(world, (world,))
     grid = Grid(dims)
@@ -388,7 +409,7 @@ def main_multi(args):
     tdt = torch.float32 if args.dtype == "f32" else torch.bfloat16
     esz = 4 if args.dtype == "f32" else 2
     ctx = RankContext(rank, grid, device=local, mode=args.mode, blocking=False)
-    host = torch.from_numpy(orc.generate_input(0, 0, rank, n, "f32")).to(tdt)
+    host = torch.from_numpy(generate_input(Workload(lengths=(n,), dtype="f32", seed=0), 0, rank, n)).to(tdt)
     pristine = host.to(dev)
     work = ctx.empty(n, args.dtype)
     scratch = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)

@@ -39,12 +39,12 @@ const void* step_kernel_i64();
 const void* step_kernel_bf16();
 const void* step_kernel_f16();
 const void* step_kernel_i32();
-const void* ll_kernel_f32();
-const void* ll_kernel_f64();
-const void* ll_kernel_i64();
-const void* ll_kernel_bf16();
-const void* ll_kernel_f16();
-const void* ll_kernel_i32();
+const void* ll_kernel_f32(int maxv);
+const void* ll_kernel_f64(int maxv);
+const void* ll_kernel_i64(int maxv);
+const void* ll_kernel_bf16(int maxv);
+const void* ll_kernel_f16(int maxv);
+const void* ll_kernel_i32(int maxv);
 }  // namespace rbx
 
 namespace {
@@ -92,6 +92,17 @@ struct CachedPlan {
   const void* local_fn = nullptr;  // specialised MODE_LOCAL kernel (rbx_local.cuh), if the shape has one
   std::shared_ptr<rbx::LocalArgs> local_args;
   int local_grid = 0;
+};
+
+struct LLKey {  // cached MODE_LL launch arguments: buffers, count, dtype
+  std::vector<void*> bufs;
+  size_t count;
+  int dtype;
+  bool operator<(const LLKey& o) const {
+    if (count != o.count) return count < o.count;
+    if (dtype != o.dtype) return dtype < o.dtype;
+    return bufs < o.bufs;
+  }
 };
 
 struct OpenedHandle {
@@ -145,6 +156,7 @@ struct rbx_comm {
   int64_t ll_oneshot_bytes = 0;
   int ll_words_per_thread = 4;        // CTAs per LL call = words / (threads * this); env RBX_LL_WPT
   int ll_coresident = 0;              // co-resident CTAs of the LL kernel
+  std::map<LLKey, std::unique_ptr<rbx::LLArgs>> ll_cache;  // per (buffers, count, dtype)
 };
 
 namespace {
@@ -184,14 +196,14 @@ const void* kernel_for(int dtype) {
   }
 }
 
-const void* ll_kernel_for(int dtype) {
+const void* ll_kernel_for(int dtype, int maxv) {
   switch (dtype) {
-    case RBX_F32: return rbx::ll_kernel_f32();
-    case RBX_F64: return rbx::ll_kernel_f64();
-    case RBX_I64: return rbx::ll_kernel_i64();
-    case RBX_BF16: return rbx::ll_kernel_bf16();
-    case RBX_F16: return rbx::ll_kernel_f16();
-    case RBX_I32: return rbx::ll_kernel_i32();
+    case RBX_F32: return rbx::ll_kernel_f32(maxv);
+    case RBX_F64: return rbx::ll_kernel_f64(maxv);
+    case RBX_I64: return rbx::ll_kernel_i64(maxv);
+    case RBX_BF16: return rbx::ll_kernel_bf16(maxv);
+    case RBX_F16: return rbx::ll_kernel_f16(maxv);
+    case RBX_I32: return rbx::ll_kernel_i32(maxv);
     default: return nullptr;
   }
 }
@@ -369,7 +381,8 @@ int check_mode_dtype(int mode, int dtype) {
 // plays (1 for a per-rank communicator, V for a virtual one).
 int ll_launch(rbx_comm* c, const std::vector<int>& ranks, void* const* bufs, size_t count, int dtype,
               cudaStream_t stream, bool cooperative) {
-  const void* fn = ll_kernel_for(dtype);
+  const int V = (int)ranks.size();
+  const void* fn = ll_kernel_for(dtype, V == 1 ? 1 : RBX_MAX_RANKS);
   if (!fn) return fail(RBX_ERR_INVALID, "unknown dtype");
   const int es = dtype_size(dtype);
   if (count * (size_t)es > (size_t)RBX_LL_MAX_BYTES)
@@ -379,50 +392,63 @@ int ll_launch(rbx_comm* c, const std::vector<int>& ranks, void* const* bufs, siz
     RBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, c->ll_threads, 0));
     c->ll_coresident = std::max(1, per_sm) * c->sm_count;
   }
-  const rbx::Geometry& g = c->geo;
-  const int m = (int)g.active_dims().size();
-  const int W = es == 8 ? 2 : 1;
-  const int64_t words = (int64_t)count * W;
-  int nb = (int)std::min<int64_t>((words + (int64_t)c->ll_threads * c->ll_words_per_thread - 1) /
-                                      ((int64_t)c->ll_threads * c->ll_words_per_thread),
-                                  (int64_t)c->nblocks);
-  if (nb < 1) nb = 1;
-  const int V = (int)ranks.size();
-  if ((int64_t)nb * V > c->ll_coresident) nb = std::max(1, c->ll_coresident / V);
-  std::unique_ptr<rbx::LLArgs> a(new rbx::LLArgs);
-  std::memset(a.get(), 0, sizeof(rbx::LLArgs));
-  a->nranks = c->nranks;
-  a->nlev = m;
-  a->nb = nb;
-  a->nhosted = V;
-  a->cap = rbx::ll_cap_words(c->nranks);
-  a->timeout_ns = c->timeout_ns;
-  a->err = c->err_dev;
-  a->trace = c->trace_dev;
-  const int64_t bytes = (int64_t)count * es;
-  a->oneshot = bytes <= c->ll_oneshot_bytes && bytes <= RBX_LL_ONESHOT_MAX_BYTES;
-  for (int q = 0; q < c->nranks; ++q) {
-    const std::vector<int> o = rbx::fold_order(g, q);
-    for (int k = 0; k < c->nranks; ++k) a->orders.of[q][k] = (uint8_t)o[k];
-  }
-  const std::vector<uint8_t> ctrl = rbx::fold_ctrl(g);
-  for (int v = 0; v < V; ++v) {
-    rbx::LLRank& R = a->rank[v];
-    const int me = ranks[v];
-    R.me = me;
-    R.buf = static_cast<char*>(bufs[v]);
-    R.my_sig = c->sig[me];
+  LLKey key{std::vector<void*>(bufs, bufs + V), count, dtype};
+  auto it = c->ll_cache.find(key);
+  if (it == c->ll_cache.end()) {
+    const rbx::Geometry& g = c->geo;
+    const int m = (int)g.active_dims().size();
+    // LL words per rank (rbx_ll.cuh LLFmt): 2-byte types pack two elements per word
+    const int64_t words = es == 2 ? ((int64_t)count + 1) / 2 : (es == 8 ? 2 * (int64_t)count : (int64_t)count);
+    int nb = (int)std::min<int64_t>((words + (int64_t)c->ll_threads * c->ll_words_per_thread - 1) /
+                                        ((int64_t)c->ll_threads * c->ll_words_per_thread),
+                                    (int64_t)c->nblocks);
+    if (nb < 1) nb = 1;
+    if ((int64_t)nb * V > c->ll_coresident) nb = std::max(1, c->ll_coresident / V);
+    std::unique_ptr<rbx::LLArgs> a(new rbx::LLArgs);
+    std::memset(a.get(), 0, sizeof(rbx::LLArgs));
+    a->nranks = c->nranks;
+    a->nlev = m;
+    a->nb = nb;
+    a->nhosted = V;
+    a->cap = rbx::ll_cap_words(c->nranks);
+    a->err = c->err_dev;
+    a->trace = c->trace_dev;
+    const int64_t bytes = (int64_t)count * es;
+    a->oneshot = bytes <= c->ll_oneshot_bytes && bytes <= RBX_LL_ONESHOT_MAX_BYTES;
     for (int q = 0; q < c->nranks; ++q) {
-      R.area[q] = c->ll_at[q];
-      rbx::region_after(g, q, (int64_t)count, m, &R.off[q], &R.len[q]);
+      const std::vector<int> o = rbx::fold_order(g, q);
+      for (int k = 0; k < c->nranks; ++k) a->orders.of[q][k] = (uint8_t)o[k];
     }
-    const std::vector<int> order = rbx::fold_order(g, me);
-    for (int k = 0; k < c->nranks; ++k) {
-      R.order[k] = (uint8_t)order[k];
-      R.ctrl[k] = ctrl[k];
+    const std::vector<uint8_t> ctrl = rbx::fold_ctrl(g);
+    for (int v = 0; v < V; ++v) {
+      rbx::LLRank& R = a->rank[v];
+      const int me = ranks[v];
+      R.me = me;
+      R.buf = static_cast<char*>(bufs[v]);
+      R.my_sig = c->sig[me];
+      for (int q = 0; q < c->nranks; ++q) {
+        R.area[q] = c->ll_at[q];
+        rbx::region_after(g, q, (int64_t)count, m, &R.off[q], &R.len[q]);
+      }
+      const std::vector<int> order = rbx::fold_order(g, me);
+      for (int k = 0; k < c->nranks; ++k) {
+        R.order[k] = (uint8_t)order[k];
+        R.ctrl[k] = ctrl[k];
+      }
     }
+    if (c->ll_cache.size() >= 4096) c->ll_cache.clear();  // bound host memory (~8 KB per entry)
+    it = c->ll_cache.emplace(std::move(key), std::move(a)).first;
   }
-  void* params[] = {a.get()};
+  rbx::LLArgs* a = it->second.get();
+  a->timeout_ns = c->timeout_ns;
+  const int nb = a->nb;
+  void* params[] = {a};
+  rbx::LLArgsT<1> a1;  // per-rank form: the same fields with one hosted rank
+  if (V == 1) {
+    std::memcpy(&a1, a, offsetof(rbx::LLArgs, rank));
+    a1.rank[0] = a->rank[0];
+    params[0] = &a1;
+  }
   dim3 grid((unsigned)(nb * V)), block((unsigned)c->ll_threads);
   if (cooperative) {
     RBX_CUDA(cudaLaunchCooperativeKernel(fn, grid, block, params, 0, stream));

@@ -6,7 +6,10 @@
 
 namespace rbx {
 const void* step_kernel_f16() { return reinterpret_cast<const void*>(&rbx_step_kernel<__half>); }
-const void* ll_kernel_f16() { return reinterpret_cast<const void*>(&rbx_ll_kernel<__half>); }
+const void* ll_kernel_f16(int maxv) {
+  return maxv == 1 ? reinterpret_cast<const void*>(&rbx_ll_kernel<__half, 1>)
+                   : reinterpret_cast<const void*>(&rbx_ll_kernel<__half, RBX_MAX_RANKS>);
+}
 
 const void* local_kernel_f16(int v, int nlev) {
 #define RBX_LOCAL_CASE(V, L) \

@@ -6,7 +6,10 @@
 
 namespace rbx {
 const void* step_kernel_f64() { return reinterpret_cast<const void*>(&rbx_step_kernel<double>); }
-const void* ll_kernel_f64() { return reinterpret_cast<const void*>(&rbx_ll_kernel<double>); }
+const void* ll_kernel_f64(int maxv) {
+  return maxv == 1 ? reinterpret_cast<const void*>(&rbx_ll_kernel<double, 1>)
+                   : reinterpret_cast<const void*>(&rbx_ll_kernel<double, RBX_MAX_RANKS>);
+}
 
 const void* local_kernel_f64(int v, int nlev) {
 #define RBX_LOCAL_CASE(V, L) \

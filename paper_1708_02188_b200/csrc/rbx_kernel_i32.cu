@@ -6,7 +6,10 @@
 
 namespace rbx {
 const void* step_kernel_i32() { return reinterpret_cast<const void*>(&rbx_step_kernel<unsigned int>); }
-const void* ll_kernel_i32() { return reinterpret_cast<const void*>(&rbx_ll_kernel<unsigned int>); }
+const void* ll_kernel_i32(int maxv) {
+  return maxv == 1 ? reinterpret_cast<const void*>(&rbx_ll_kernel<unsigned int, 1>)
+                   : reinterpret_cast<const void*>(&rbx_ll_kernel<unsigned int, RBX_MAX_RANKS>);
+}
 
 const void* local_kernel_i32(int v, int nlev) {
 #define RBX_LOCAL_CASE(V, L) \

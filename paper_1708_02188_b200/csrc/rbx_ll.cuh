@@ -64,17 +64,22 @@ struct LLOrders {  // one-shot: the fold order of every owner's region
   uint8_t of[RBX_MAX_RANKS][RBX_MAX_RANKS];
 };
 
-struct LLArgs {
+// MAXV: ranks hosted by one launch (1 for a per-rank communicator, up to 16 for
+// a virtual one).  The per-rank form keeps the kernel parameters under 1 KB;
+// the 16-rank form is ~7.5 KB, which measurably slows the host-side launch.
+template <int MAXV>
+struct LLArgsT {
   int nranks, nlev, nb;  // nb CTAs per rank
-  int nhosted;           // ranks hosted by this launch (1, or V for a virtual communicator)
+  int nhosted;           // ranks hosted by this launch
   int oneshot;           // 1: one-shot variant
   int64_t cap;           // words per slot
   uint64_t timeout_ns;
   ErrRecord* err;
   unsigned long long* trace;  // optional timeline (RBX_TRACE), same slots as rbx_step_kernel
   LLOrders orders;
-  LLRank rank[RBX_MAX_RANKS];
+  LLRank rank[MAXV];
 };
+using LLArgs = LLArgsT<RBX_MAX_RANKS>;
 
 __device__ __forceinline__ void st_ll(unsigned long long* p, uint32_t data, uint32_t e) {
   const unsigned long long v = ((unsigned long long)e << 32) | data;
@@ -213,8 +218,8 @@ __device__ __forceinline__ void ll_fold_unit(const LLRank& R, const uint8_t* ord
   F::pack(r, res);
 }
 
-template <typename T>
-__global__ void __launch_bounds__(512, 1) rbx_ll_kernel(const __grid_constant__ LLArgs a) {
+template <typename T, int MAXV>
+__global__ void __launch_bounds__(512, 1) rbx_ll_kernel(const __grid_constant__ LLArgsT<MAXV> a) {
   using F = LLFmt<T>;
   constexpr int WPU = F::WPU;
   constexpr int U = 4;  // words per thread in flight (scatter / gather)
