@@ -157,6 +157,11 @@ struct rbx_comm {
   int ll_words_per_thread = 4;        // CTAs per LL call = words / (threads * this); env RBX_LL_WPT
   int ll_coresident = 0;              // co-resident CTAs of the LL kernel
   std::map<LLKey, std::unique_ptr<rbx::LLArgs>> ll_cache;  // per (buffers, count, dtype)
+  // Launches of one communicator share a device epoch, so they must not overlap:
+  // a launch on a different stream than the previous one waits for it.
+  cudaEvent_t order_ev = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool has_last = false;
 };
 
 namespace {
@@ -347,6 +352,26 @@ int upload(rbx_comm* c, std::vector<rbx::Plan>& host, const std::vector<std::vec
   return RBX_OK;
 }
 
+// Serialise launches of one communicator across streams (outside stream
+// capture; inside a graph the capture order is the user's contract).
+int order_before(rbx_comm* c, cudaStream_t stream, bool* capturing) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  RBX_CUDA(cudaStreamIsCapturing(stream, &st));
+  *capturing = st != cudaStreamCaptureStatusNone;
+  if (*capturing) return RBX_OK;
+  if (!c->order_ev) RBX_CUDA(cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming));
+  if (c->has_last && stream != c->last_stream) RBX_CUDA(cudaStreamWaitEvent(stream, c->order_ev, 0));
+  return RBX_OK;
+}
+
+int order_after(rbx_comm* c, cudaStream_t stream, bool capturing) {
+  if (capturing) return RBX_OK;
+  RBX_CUDA(cudaEventRecord(c->order_ev, stream));
+  c->last_stream = stream;
+  c->has_last = true;
+  return RBX_OK;
+}
+
 int launch(rbx_comm* c, const CachedPlan& cp, int dtype, cudaStream_t stream, bool cooperative, int nblocks) {
   const void* fn = kernel_for(dtype);
   if (!fn) return fail(RBX_ERR_INVALID, "unknown dtype");
@@ -360,13 +385,15 @@ int launch(rbx_comm* c, const CachedPlan& cp, int dtype, cudaStream_t stream, bo
   void* params[] = {&a};
   dim3 grid((unsigned)(nblocks * cp.nplans)), block((unsigned)c->threads);
   const size_t smem = (size_t)((cp.plan_bytes + 15) / 16 * 16);
+  bool capturing = false;
+  if (int rc = order_before(c, stream, &capturing)) return rc;
   if (cooperative) {
     RBX_CUDA(cudaLaunchCooperativeKernel(fn, grid, block, params, smem, stream));
   } else {
     RBX_CUDA(cudaLaunchKernel(fn, grid, block, params, smem, stream));
   }
   c->launches++;
-  return RBX_OK;
+  return order_after(c, stream, capturing);
 }
 
 // Every (mode, dtype) pair is supported: RING_DIMS keeps bf16/f16 stage
@@ -450,13 +477,15 @@ int ll_launch(rbx_comm* c, const std::vector<int>& ranks, void* const* bufs, siz
     params[0] = &a1;
   }
   dim3 grid((unsigned)(nb * V)), block((unsigned)c->ll_threads);
+  bool capturing = false;
+  if (int rc = order_before(c, stream, &capturing)) return rc;
   if (cooperative) {
     RBX_CUDA(cudaLaunchCooperativeKernel(fn, grid, block, params, 0, stream));
   } else {
     RBX_CUDA(cudaLaunchKernel(fn, grid, block, params, 0, stream));
   }
   c->launches++;
-  return RBX_OK;
+  return order_after(c, stream, capturing);
 }
 
 // MODE_PUSH pointer-table entries of rank `me` for one buffer (rbx_plan.h
@@ -815,6 +844,7 @@ int rbx_comm_destroy(rbx_comm_t* c) {
     }
   }
   if (c->sig_local) cudaFree(c->sig_local);
+  if (c->order_ev) cudaEventDestroy(c->order_ev);
   if (c->inbox_owned && c->inbox_local) cudaFree(c->inbox_local);
   if (c->err_host) cudaFreeHost(c->err_host);
   delete c;

@@ -194,6 +194,37 @@ def test_ll_oneshot_and_twoshot_variants(oneshot_bytes, monkeypatch):
     del torch
 
 
+def test_launches_on_different_streams_are_serialised():
+    """Launches of one communicator share its device epoch; collectives issued
+    back to back on different streams must not overlap (the library orders
+    them), so alternating streams without any host sync stays correct."""
+    torch = _torch()
+    from paper_1708_02188_b200.virtual import VirtualRanks
+
+    dims = (2, 2, 2)
+    vr = VirtualRanks(dims, nblocks_per_rank=4)
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    rng = np.random.default_rng(8)
+    cases = []
+    for k in range(18):
+        length = int(rng.integers(1, 40_000))
+        parts = [rng.integers(-1000, 1001, length).astype(np.int64) for _ in range(8)]
+        ts = [torch.from_numpy(p).cuda() for p in parts]
+        cases.append((parts, ts))
+    torch.cuda.synchronize()
+    for k, (parts, ts) in enumerate(cases):
+        st = streams[k % 3]
+        st.wait_stream(torch.cuda.current_stream())
+        vr.collective(ts, mode=["ll", "fused", "ring_dims"][k % 3], stream=st)
+    torch.cuda.synchronize()
+    vr.check()
+    for parts, ts in cases:
+        want = np.sum(parts, axis=0)
+        for t in ts:
+            assert np.array_equal(t.cpu().numpy(), want)
+    vr.close()
+
+
 def test_ll_limits_and_large_ragged_inputs():
     """MODE_LL (8-byte {data, epoch} words, no flags): every size up to its
     1 MiB-per-rank cap is bit-exact, and a larger buffer is refused, not truncated."""
