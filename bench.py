@@ -56,8 +56,13 @@ def parse_args():
     p.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-nccl", action="store_true")
-    p.add_argument("--e2e-chunks", type=int, default=8, help="pipeline windows for the host-buffer e2e leg")
-    return p.parse_args()
+    p.add_argument("--e2e-chunks", type=int, default=None,
+                   help="pipeline windows for the host-buffer e2e leg (default 8 at N=1, 32 at N>1: "
+                        "best measured against the host PCIe ceiling, profiles/r01_pcie_probe_*gpu.jsonl)")
+    a = p.parse_args()
+    if a.e2e_chunks is None:
+        a.e2e_chunks = 8 if a.gpus == 1 else 32
+    return a
 
 
 def hbm_peak():

@@ -128,10 +128,13 @@ struct rbx_comm {
   bool connected = false;
   int sm_count = 148;
   int max_coresident = 0;  // co-resident CTAs of the step kernel
-  // work tile in 16-byte vectors (0: contiguous range per CTA); env RBX_TILE.  -1 = by dtype:
-  // 1024 for 4/8-byte types, 2048 for bf16/f16, whose heavier fold (unpack, fp32 add, RNE)
-  // needs more vectors in flight per call (N=2 bf16 +5.5 %, fp32 flat; profiles/r01_tile_by_dtype.txt)
+  // work tile in 16-byte vectors (0: contiguous range per CTA); env RBX_TILE.  -1 = default:
+  // 2048 with dynamic tiles; with static tiles 1024 for 4/8-byte types and 2048 for bf16/f16, whose
+  // heavier fold needs more vectors in flight per call (profiles/r01_tile_by_dtype.txt)
   int tile = -1;
+  // dynamic work tiles (claimed from a per-step counter); env RBX_DYN.  With 2048-vector tiles
+  // N=2 581 -> 595 GB/s, N=4 578 -> 597 GB/s busbw at 102.4 MB fp32 (profiles/r01_dyn_tiles_4gpu.txt)
+  int dyn_tiles = 1;
   int local_tile = 2048;   // same for the HBM-bound local mode (measured best of 0/512/2048/4096/8192/32768); env RBX_LOCAL_TILE
   size_t bytes_per_cta = 32 * 1024;   // adaptive CTA count per call; env RBX_BYTES_PER_CTA
   int min_blocks = 16;                // env RBX_MIN_BLOCKS
@@ -289,6 +292,7 @@ int common_init(rbx_comm* c, const int* dims, int ndims, int device, int threads
   c->device = device;
   if (const char* t = std::getenv("RBX_TILE")) c->tile = std::atoi(t);
   if (const char* t = std::getenv("RBX_LOCAL_TILE")) c->local_tile = std::atoi(t);
+  if (const char* t = std::getenv("RBX_DYN")) c->dyn_tiles = std::atoi(t);
   if (const char* t = std::getenv("RBX_LOCAL_GENERIC")) c->local_specialised = std::atoi(t) == 0;
   if (const char* t = std::getenv("RBX_LOCAL_CTAS_PER_SM")) c->local_ctas_per_sm = std::atoi(t);
   if (const char* t = std::getenv("RBX_BYTES_PER_CTA")) c->bytes_per_cta = (size_t)std::max(1L, std::atol(t));
@@ -340,7 +344,8 @@ int upload(rbx_comm* c, std::vector<rbx::Plan>& host, const std::vector<std::vec
   for (size_t i = 0; i < host.size(); ++i) {
     rbx::Plan& p = host[i];
     p.ptrs = out->ptrs + (tables.size() == host.size() ? base[i] : 0);
-    p.tile = p.nosync ? c->local_tile : (c->tile >= 0 ? c->tile : (dtype_size(dtype) == 2 ? 2048 : 1024));
+    p.tile = p.nosync ? c->local_tile : (c->tile >= 0 ? c->tile : (c->dyn_tiles || dtype_size(dtype) == 2 ? 2048 : 1024));
+    p.dyn = (!p.nosync && p.tile > 0) ? c->dyn_tiles : 0;
     int segs = 0;
     for (int s = 0; s < p.nsteps; ++s) segs += p.steps[s].nseg;
     if (segs > maxsegs) maxsegs = segs;

@@ -518,7 +518,8 @@ __host__ __device__ constexpr size_t plan_smem_bytes(int nsegs) {
 // CTAs (tile == 0: one contiguous range per CTA).
 template <typename T>
 __device__ __forceinline__ void run_step_work(const Plan& P, const Step& st, int b, int nb, SegCtx& s_seg,
-                                              int& s_cur /* thread-local: same value in every thread */) {
+                                              int& s_cur /* thread-local: same value in every thread */,
+                                              unsigned int* tile_ctr, int* s_next) {
   const int64_t T_vec = st.total_vec;
   auto setup = [&](int k) {
     const Seg& sg = P.segs[st.seg0 + k];
@@ -557,6 +558,24 @@ __device__ __forceinline__ void run_step_work(const Plan& P, const Step& st, int
   if (P.tile <= 0) {
     const int64_t my0 = T_vec * b / nb, my1 = T_vec * (b + 1) / nb;
     if (my0 < my1) body(my0, my1);
+  } else if (tile_ctr && (T_vec + P.tile - 1) / P.tile > nb) {
+    // Dynamic tiles: CTA b starts with tile b, then claims tiles nb, nb+1, ...
+    // from this step's counter.  The claim for the next tile is issued before
+    // the current tile's loads, so its latency hides under them; CTAs that
+    // get more NVLink bandwidth simply take more tiles (no fixed tail).
+    const int64_t tile = P.tile;
+    const int64_t ntiles = (T_vec + tile - 1) / tile;
+    int64_t t = b;
+    while (t < ntiles) {
+      unsigned int nxt = 0;
+      if (threadIdx.x == 0) nxt = (unsigned)nb + atomicAdd(tile_ctr, 1u);
+      const int64_t lo = t * tile;
+      body(lo, lo + tile < T_vec ? lo + tile : T_vec);
+      __syncthreads();  // every thread has read *s_next for this tile
+      if (threadIdx.x == 0) *s_next = (int)nxt;
+      __syncthreads();
+      t = *s_next;
+    }
   } else {
     const int64_t tile = P.tile;
     for (int64_t t = b; t * tile < T_vec; t += nb) {
@@ -590,6 +609,7 @@ __global__ void __launch_bounds__(512, 1) rbx_step_kernel(KernelArgs args) {
   __shared__ uint32_t s_epoch;
   __shared__ int s_fail;
   __shared__ SegCtx s_seg;
+  __shared__ int s_next;
   // optional timeline (RBX_TRACE): first and last CTA of the first rank
   unsigned long long* tr = nullptr;
   if (args.trace && threadIdx.x == 0 && vrank == 0 && (b == 0 || b == nb - 1)) tr = args.trace + (b == 0 ? 0 : 32);
@@ -659,7 +679,9 @@ __global__ void __launch_bounds__(512, 1) rbx_step_kernel(KernelArgs args) {
     // ---- work ----
     if (st.nseg) {
       int cur = -1;  // segment whose pointers are in s_seg (thread-local, uniform)
-      run_step_work<T>(P, st, b, nb, s_seg, cur);
+      unsigned int* ctr = (P.dyn && !P.nosync && P.tile > 0)
+                              ? reinterpret_cast<unsigned int*>(my_sig + SigLayout::tiles_off + s) : nullptr;
+      run_step_work<T>(P, st, b, nb, s_seg, cur, ctr, &s_next);
     }
     if (tr && s < 9) tr[4 + 3 * s] = global_ns();
     // ---- signal ----
@@ -683,6 +705,8 @@ __global__ void __launch_bounds__(512, 1) rbx_step_kernel(KernelArgs args) {
       unsigned int* done = reinterpret_cast<unsigned int*>(my_sig + SigLayout::epoch_off + 1);
       if (atomicAdd(done, 1u) == (unsigned)nb - 1u) {
         *done = 0u;
+        if (P.dyn)  // every CTA has made its last claim: rewind the tile counters
+          for (int s = 0; s < P.nsteps; ++s) my_sig[SigLayout::tiles_off + s] = 0u;
         *(volatile uint32_t*)(my_sig + SigLayout::epoch_off) = e;
       }
     }

@@ -75,10 +75,11 @@ struct Step {
 };
 
 // Device-resident plan of ONE rank.  Pointers are filled in by the runtime.
-struct Plan {
+struct alignas(16) Plan {  // 16-byte multiple: plans[v] is staged with int4 loads
   int32_t me, nranks, nsteps, nentry;
   int32_t nosync, vec;     // vec = elements per 16-byte vector for this dtype
   int32_t nblocks, tile;   // tile: vectors per round-robin work tile (0 = one contiguous range per CTA)
+  int32_t dyn, pad_;       // dyn: after its first tile a CTA claims the next tile from a per-step counter
   uint8_t entry_peers[RBX_MAX_RANKS];
   uint32_t* sig[RBX_MAX_RANKS];   // signal area of every rank (mapped)
   uint32_t* my_sig;               // == sig[me]
@@ -89,10 +90,13 @@ struct Plan {
   Seg segs[RBX_MAX_SEGS];
 };
 
+static_assert(sizeof(Plan) % 16 == 0, "plans are staged into shared memory with 16-byte loads");
+
 // Signal-area layout (uint32 words) of one rank.
 struct SigLayout {
   static constexpr int64_t flags_words = (int64_t)RBX_NSLOTS * RBX_MAX_RANKS * RBX_MAX_BLOCKS;
-  static constexpr int64_t epoch_off = flags_words;            // epoch[RBX_MAX_BLOCKS]
+  static constexpr int64_t epoch_off = flags_words;            // epoch[RBX_MAX_BLOCKS]: [0] epoch, [1] exit count
+  static constexpr int64_t tiles_off = epoch_off + 16;         // per-step tile counters (dynamic work tiles)
   static constexpr int64_t abort_off = epoch_off + RBX_MAX_BLOCKS;
   static constexpr int64_t words = abort_off + 32;
   static constexpr int64_t bytes = words * 4;
