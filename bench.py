@@ -502,6 +502,7 @@ def main_multi(args):
         dist.all_reduce(ntt, op=dist.ReduceOp.MAX)
         nccl = round(busbw(world, nbytes, ntt.median().item() / 1e3), 2)
 
+    traffic = ncu_traffic("nvlink_tx_2_25.6M_f32") if (world == 2 and n == N_ELEM and args.dtype == "f32") else None
     if rank == 0:
         line = {
             "metric": "multi-ring allreduce bus GB/s vs msg size at 2/4/8 B200; % of 900 GB/s NVLink",
@@ -515,7 +516,9 @@ def main_multi(args):
             "busbw_gbs": round(bw, 3), "pct_of_900": round(100 * bw / NOMINAL_NVLINK_GBS, 2),
             "algbw_gbs": round(nbytes / t / 1e9, 3),
             "roofline": {"bound": "nvlink", "achieved": round(bw, 2), "peak": MEASURED_PEER_GBS, "unit": "GB/s",
-                         "frac": round(bw / MEASURED_PEER_GBS, 4), "traffic": None,
+                         "frac": round(bw / MEASURED_PEER_GBS, 4), "traffic": traffic,
+                         "traffic_kind": "NVLink TX bytes per launch per GPU (ncu nvltx__bytes.sum, user + protocol; "
+                                         "2-GPU harness, profiles/ncu_traffic.json)" if traffic else None,
                          "peak_source": "measured peer copy per direction (B200_PROFILING.md); nominal 900",
                          "algorithmic_bytes_per_launch": int(2 * (world - 1) / world * nbytes)},
             "nccl_busbw_gbs": nccl,

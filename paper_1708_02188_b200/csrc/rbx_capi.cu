@@ -129,7 +129,7 @@ struct rbx_comm {
   int sm_count = 148;
   int max_coresident = 0;  // co-resident CTAs of the step kernel
   // work tile in 16-byte vectors (0: contiguous range per CTA); env RBX_TILE.  -1 = default:
-  // 2048 with dynamic tiles; with static tiles 1024 for 4/8-byte types and 2048 for bf16/f16, whose
+  // pass_tile() with dynamic tiles; with static tiles 1024 for 4/8-byte types and 2048 for bf16/f16, whose
   // heavier fold needs more vectors in flight per call (profiles/r01_tile_by_dtype.txt)
   int tile = -1;
   // dynamic work tiles (claimed from a per-step counter); env RBX_DYN.  With 2048-vector tiles
@@ -327,6 +327,24 @@ std::string plan_key(int op, int mode, int dtype, const std::vector<const void*>
   return k;
 }
 
+// Default work tile with dynamic tiles: one pass of the fold loop, i.e. threads x U vectors,
+// where U is fold_body's unroll for the plan's widest fold (rbx_kernel.cuh).  A smaller tile
+// leaves loads of the pass unissued (N=2, tile 512: 503 vs 595 GB/s); a larger one coarsens
+// the tail.  fp32: N=2 -> 2048, (2,2) -> 1024, (2,2,2) -> 512.
+int pass_tile(const rbx::Plan& p, int threads) {
+  int u = 0;
+  for (int s = 0; s < p.nsteps; ++s)
+    for (int k = 0; k < p.steps[s].nseg; ++k) {
+      const rbx::Seg& sg = p.segs[p.steps[s].seg0 + k];
+      if (sg.nsrc < 2 || sg.acc) continue;
+      const int B = sg.nsrc < 8 ? sg.nsrc : 8;
+      const int u_ld = std::max(1, RBX_LD_DEPTH / B);
+      const int u_acc = std::max(1, 32 / (std::max(1, (int)sg.nlev) * p.vec));
+      u = std::max(u, std::min(u_ld, u_acc));
+    }
+  return u ? threads * u : 2048;
+}
+
 // tables: one pointer table shared by every plan, or one per plan (MODE_PUSH
 // tables depend on the rank: own inbox slots, this rank's slot in the peers').
 int upload(rbx_comm* c, std::vector<rbx::Plan>& host, const std::vector<std::vector<void*>>& tables,
@@ -344,7 +362,12 @@ int upload(rbx_comm* c, std::vector<rbx::Plan>& host, const std::vector<std::vec
   for (size_t i = 0; i < host.size(); ++i) {
     rbx::Plan& p = host[i];
     p.ptrs = out->ptrs + (tables.size() == host.size() ? base[i] : 0);
-    p.tile = p.nosync ? c->local_tile : (c->tile >= 0 ? c->tile : (c->dyn_tiles || dtype_size(dtype) == 2 ? 2048 : 1024));
+    if (p.nosync)
+      p.tile = c->local_tile;
+    else if (c->tile >= 0)
+      p.tile = c->tile;
+    else
+      p.tile = c->dyn_tiles ? pass_tile(p, c->threads) : (dtype_size(dtype) == 2 ? 2048 : 1024);
     p.dyn = (!p.nosync && p.tile > 0) ? c->dyn_tiles : 0;
     int segs = 0;
     for (int s = 0; s < p.nsteps; ++s) segs += p.steps[s].nseg;
