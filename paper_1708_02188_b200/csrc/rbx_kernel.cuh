@@ -623,9 +623,11 @@ __global__ void __launch_bounds__(512, 1) rbx_step_kernel(KernelArgs args) {
     int4* dst = reinterpret_cast<int4*>(s_plan_raw);
     const int words = (int)((args.plan_bytes + 15) / 16);
     for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = __ldg(src + i);
+    if (tr) tr[20] = global_ns();  // slots 20-24: prologue detail (plans of <= 5 steps)
   }
   const Plan& P = *reinterpret_cast<const Plan*>(s_plan_raw);
   __syncthreads();
+  if (tr) tr[21] = global_ns();
   uint32_t* my_sig = P.my_sig;
   volatile uint32_t* abort_word = my_sig ? (volatile uint32_t*)(my_sig + SigLayout::abort_off) : nullptr;
   const uint64_t t0 = P.nosync ? 0 : global_ns();
@@ -635,6 +637,7 @@ __global__ void __launch_bounds__(512, 1) rbx_step_kernel(KernelArgs args) {
     // one epoch per rank (all CTAs of a launch agree; launches on a stream are
     // ordered, so the previous launch's final increment is visible here)
     s_epoch = P.nosync ? 0u : *(volatile uint32_t*)(my_sig + SigLayout::epoch_off) + 1u;
+    if (tr) tr[22] = global_ns();
   }
   __syncthreads();
   const uint32_t e = s_epoch;
@@ -648,6 +651,7 @@ __global__ void __launch_bounds__(512, 1) rbx_step_kernel(KernelArgs args) {
     st_relaxed_sys(P.sig[q] + flag_index(0, P.me, b), e);
   }
   if (tr) tr[2] = global_ns();
+  if (tr) tr[23] = global_ns();
 
   for (int s = 0; s < P.nsteps; ++s) {
     const Step& st = P.steps[s];
