@@ -1,0 +1,27 @@
+"""Host side of MultiringDataParallel (paper_1708_02188_b200/dp.py): the
+bucket assignment reproduces DDP's 25 MiB bucketing of ResNet-50/101
+(the config-4/5 bucket lists)."""
+
+import pytest
+
+from paper_1708_02188_b200.dp import ddp_bucket_assignment
+
+
+def test_bucket_assignment_rules():
+    mb = 1 << 20
+    # first bucket closes at 1 MiB, later ones at the cap; a bucket closes once it reaches its cap
+    assert ddp_bucket_assignment([mb // 2, mb // 2, mb, 3 * mb], mb, 2 * mb) == [[0, 1], [2, 3]]
+    assert ddp_bucket_assignment([], mb, 2 * mb) == []
+    assert ddp_bucket_assignment([10], mb, 2 * mb) == [[0]]
+
+
+@pytest.mark.parametrize("name,want", [
+    ("resnet50", [2_049_000, 7_875_584, 6_563_840, 6_637_568, 2_431_040]),
+    ("resnet101", [2_049_000, 7_875_584, 6_563_840, 6_965_760, 6_703_104, 6_703_104, 6_590_464, 1_098_304]),
+])
+def test_resnet_buckets_match_ddp(name, want):
+    torchvision = pytest.importorskip("torchvision")
+    m = getattr(torchvision.models, name)(num_classes=1000)
+    order = list(reversed(list(m.parameters())))
+    got = [sum(order[i].numel() for i in b) for b in ddp_bucket_assignment([p.numel() * 4 for p in order])]
+    assert got == want
