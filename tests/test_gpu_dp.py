@@ -1,5 +1,5 @@
-"""MultiringDataParallel (paper_1708_02188_b200/dp.py) on 2 GPUs: gradients
-reduced bucket by bucket from autograd hooks, in the gradient arena, are
+"""MultiringDataParallel (paper_1708_02188_b200/dp.py) on 2 and 4 GPUs (grids
+(2,) and (2,2)): gradients reduced bucket by bucket from autograd hooks, in the gradient arena, are
 bit-identical to the reference's allreduce of every bucket (oracle closed form
 over all ranks' local gradients, one allreduce per bucket as with
 Workload.lengths, runtime.py:390-398) times 1/N; the same step captured into a
@@ -62,7 +62,8 @@ def _main(rank, world, port, q):
             p.grad = torch.zeros_like(p)
         loss_of(plain).backward()
 
-        ctx = RankContext(rank, Grid((world,)), group=gloo, device=rank, blocking=False)
+        dims = {2: (2,), 4: (2, 2)}[world]
+        ctx = RankContext(rank, Grid(dims), group=gloo, device=rank, blocking=False)
         model = _model(dev)
         dp = MultiringDataParallel(model, ctx, bucket_cap_mb=0.5, first_bucket_mb=0.25)
         nb = len(dp.buckets)
@@ -82,7 +83,7 @@ def _main(rank, world, port, q):
         dist.all_gather_object(parts, local, group=gloo)
         want = np.empty_like(local)
         for lo, hi in dp.ranges:
-            red = orc.closed_form_allreduce(orc.Grid((world,)), [pt[lo:hi] for pt in parts])
+            red = orc.closed_form_allreduce(orc.Grid(dims), [pt[lo:hi] for pt in parts])
             want[lo:hi] = red * np.float32(1.0 / world)
         exact = bool(np.array_equal(got.view(np.uint32), want.view(np.uint32)))
 
@@ -117,18 +118,19 @@ def _main(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_dp_buckets_bit_exact_and_graph_replay():
-    if cuda_count() < 2:
-        pytest.skip("needs 2 GPUs")
+@pytest.mark.parametrize("world", [2, 4])
+def test_dp_buckets_bit_exact_and_graph_replay(world):
+    if cuda_count() < world:
+        pytest.skip(f"needs {world} GPUs")
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_main, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_main, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = sorted(q.get(timeout=600) for _ in range(2))
+    res = sorted(q.get(timeout=600) for _ in range(world))
     for p in procs:
         p.join(timeout=60)
     for rank, status, exact, graph_same, close, nb, launched in res:
