@@ -42,6 +42,7 @@ NOMINAL_NVLINK_GBS = 900.0
 MEASURED_PEER_GBS = 770.0  # B200_PROFILING.md: measured peer copy per direction (NVLink reference)
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
 DIMS_FOR = {1: (2, 2, 2), 2: (2,), 4: (2, 2), 8: (2, 2, 2)}
+SPIN_CYCLES = int(os.environ.get("BENCH_SPIN_CYCLES", "1000000"))
 
 
 def parse_args():
@@ -200,9 +201,10 @@ def flush_l2(scratch):
 
     scratch.fill_(1.0)
     scratch.sum()
-    # ~50 us of device spin so the host enqueues the timed launch before the GPU
-    # gets there: the events then time the kernel, not Python launch latency
-    torch.cuda._sleep(100_000)
+    # device spin (default 1M cycles, ~0.5 ms; env BENCH_SPIN_CYCLES) so the host
+    # enqueues the timed launch before the GPU gets there: the events then time
+    # the kernel, not Python launch latency
+    torch.cuda._sleep(SPIN_CYCLES)
 
 
 def workload_name(n: int, dtype: str, ranks: int, dims) -> str:
