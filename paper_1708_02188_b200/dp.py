@@ -31,6 +31,7 @@ instead of the multi-ring kernel (comparison only).
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 
 
@@ -96,6 +97,7 @@ class MultiringDataParallel:
         self.stream = torch.cuda.Stream(device=dev)
         self._launch_args = {}
         self._armed = False
+        self._sync = True
         self._pending = []
         self._next = 0
         self.launched = 0
@@ -110,9 +112,22 @@ class MultiringDataParallel:
         do not use optimizer.zero_grad(set_to_none=True))."""
         self.arena.zero_()
 
+    @contextlib.contextmanager
+    def no_sync(self):
+        """Accumulate gradients locally (no bucket allreduces) for the backward
+        passes inside the block, like DDP.no_sync(); the first backward after it
+        reduces the accumulated gradients."""
+        prev, self._sync = self._sync, False
+        try:
+            yield
+        finally:
+            self._sync = prev
+
     def _on_grad(self, p) -> None:
         import torch
 
+        if not self._sync:
+            return
         if not self._armed:
             self._armed = True
             self._pending = [len(b) for b in self.buckets]

@@ -87,6 +87,17 @@ def _main(rank, world, port, q):
             want[lo:hi] = red * np.float32(1.0 / world)
         exact = bool(np.array_equal(got.view(np.uint32), want.view(np.uint32)))
 
+        # no_sync(): the first backward accumulates locally, the second reduces the sum
+        # (2x every local gradient: exactly twice the reduced bits, x2 commutes with RNE)
+        dp.zero_grad()
+        with dp.no_sync():
+            loss_of(dp).backward()
+        loss_of(dp).backward()
+        torch.cuda.synchronize()
+        exact = exact and bool(np.array_equal(dp.arena.cpu().numpy().view(np.uint32),
+                                              (got * np.float32(2)).view(np.uint32)))
+        launched_twice = dp.launched == 2 * len(dp.buckets)
+
         # the same step captured into a CUDA graph and replayed
         def step():
             dp.zero_grad()
@@ -109,7 +120,7 @@ def _main(rank, world, port, q):
         close = bool(np.allclose(dp2.arena.cpu().numpy(), got, rtol=1e-5, atol=1e-7))
         dp2.close()
         ctx.close()
-        q.put((rank, "ok", exact, graph_same, close, nb, launched))
+        q.put((rank, "ok", exact, graph_same, close, nb, launched if launched_twice else -1))
     except Exception as exc:  # noqa: BLE001
         import traceback
 
