@@ -19,6 +19,8 @@ physical GPUs (N * busbw; at N = 1 the single GPU's busbw).  Every step
 restores the inputs and flushes L2 (256 MiB write, read back so no dirty
 lines are charged to the kernel) outside the timed region; the timed region
 is one allreduce, CUDA events on the launching stream, max over ranks.
+At N > 1 the line also carries `curve`: busbw at 4 KB, 64 KB, 1 MB, 16 MB,
+256 MB and 1 GiB per rank (the metric's "vs msg size"), timed the same way.
 `--impl reference` runs the reference runtime's phase loop ported to C
 (oracle/rbx_oracle.c, one thread per rank) on the host on the same job.
 """
@@ -42,6 +44,7 @@ NOMINAL_NVLINK_GBS = 900.0
 MEASURED_PEER_GBS = 770.0  # B200_PROFILING.md: measured peer copy per direction (NVLink reference)
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
 DIMS_FOR = {1: (2, 2, 2), 2: (2,), 4: (2, 2), 8: (2, 2, 2)}
+CURVE_BYTES = (4096, 65536, 1 << 20, 16 << 20, 256 << 20, 1 << 30)  # N>1 busbw-vs-size points in the bench line
 SPIN_CYCLES = int(os.environ.get("BENCH_SPIN_CYCLES", "1000000"))
 
 
@@ -57,6 +60,7 @@ def parse_args():
     p.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-nccl", action="store_true")
+    p.add_argument("--curve", type=int, default=1, help="N>1: add busbw at 4 KB..1 GiB to the line")
     p.add_argument("--e2e-chunks", type=int, default=None,
                    help="pipeline windows for the host-buffer e2e leg (default 8 at N=1, 32 at N>1: "
                         "best measured against the host PCIe ceiling, profiles/r01_pcie_probe_*gpu.jsonl)")
@@ -481,6 +485,33 @@ def main_multi(args):
     t_e2e = e2e_t.mean().item() / 1e3
     ctx.check()
 
+    # the metric's "vs msg size" curve: the same timing (L2 flushed, device barrier,
+    # one collective between events, max over ranks) on views of one large buffer
+    curve = []
+    if args.curve:
+        big_n = max(CURVE_BYTES) // esz
+        big = ctx.empty(big_n, args.dtype)
+        big.fill_(1.0)
+        for nbytes_c in CURVE_BYTES:
+            view = big[:nbytes_c // esz]
+            ts = []
+            for it in range(3 + 10):
+                flush_l2(scratch)
+                ctx.barrier()
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record(stream)
+                ctx.collective("allreduce", view)
+                e.record(stream)
+                torch.cuda.synchronize()
+                if it >= 3:
+                    ts.append(s.elapsed_time(e))
+            tt = torch.tensor(ts, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            us = tt.median().item() * 1e3
+            curve.append({"bytes": nbytes_c, "us": round(us, 2), "busbw_gbs": round(busbw(world, nbytes_c, us / 1e6), 2)})
+        ctx.check()
+        del big
+
     nccl = None
     if not args.no_nccl:
         nbuf = pristine.clone()
@@ -524,6 +555,7 @@ def main_multi(args):
                          "peak_source": "measured peer copy per direction (B200_PROFILING.md); nominal 900",
                          "algorithmic_bytes_per_launch": int(2 * (world - 1) / world * nbytes)},
             "nccl_busbw_gbs": nccl,
+            "curve": curve or None,
             "cpu_baseline": None,
             "e2e": {"value": round(busbw(world, nbytes, t_e2e) * world, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": round(t_e2e * 1e3, 3),
