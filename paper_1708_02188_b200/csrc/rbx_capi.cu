@@ -327,21 +327,26 @@ std::string plan_key(int op, int mode, int dtype, const std::vector<const void*>
   return k;
 }
 
-// Default work tile with dynamic tiles: one pass of the fold loop, i.e. threads x U vectors,
-// where U is fold_body's unroll for the plan's widest fold (rbx_kernel.cuh).  A smaller tile
-// leaves loads of the pass unissued (N=2, tile 512: 503 vs 595 GB/s); a larger one coarsens
-// the tail.  fp32: N=2 -> 2048, (2,2) -> 1024, (2,2,2) -> 512.
-int pass_tile(const rbx::Plan& p, int threads) {
+// Default work tile of step s with dynamic tiles: one pass of the fold loop, i.e. threads x U
+// vectors, where U is fold_body's unroll for the step's widest fold (rbx_kernel.cuh; 8 for a
+// copy step).  A smaller tile leaves loads of the pass unissued (N=2, tile 512: 503 vs 595
+// GB/s); a larger one coarsens the tail.  fp32 FUSED: N=2 -> 2048, (2,2) -> 1024, (2,2,2) -> 512.
+int pass_tile(const rbx::Plan& p, int s, int threads) {
   int u = 0;
-  for (int s = 0; s < p.nsteps; ++s)
-    for (int k = 0; k < p.steps[s].nseg; ++k) {
-      const rbx::Seg& sg = p.segs[p.steps[s].seg0 + k];
-      if (sg.nsrc < 2 || sg.acc) continue;
+  for (int k = 0; k < p.steps[s].nseg; ++k) {
+    const rbx::Seg& sg = p.segs[p.steps[s].seg0 + k];
+    if (sg.acc) continue;
+    int us;
+    if (sg.nsrc < 2) {
+      us = 8;  // copy (REPLACE): fold_body<T,1,L> keeps 8 loads in flight per thread
+    } else {
       const int B = sg.nsrc < 8 ? sg.nsrc : 8;
       const int u_ld = std::max(1, RBX_LD_DEPTH / B);
       const int u_acc = std::max(1, 32 / (std::max(1, (int)sg.nlev) * p.vec));
-      u = std::max(u, std::min(u_ld, u_acc));
+      us = std::min(u_ld, u_acc);
     }
+    u = std::max(u, us);
+  }
   return u ? threads * u : 2048;
 }
 
@@ -367,7 +372,9 @@ int upload(rbx_comm* c, std::vector<rbx::Plan>& host, const std::vector<std::vec
     else if (c->tile >= 0)
       p.tile = c->tile;
     else
-      p.tile = c->dyn_tiles ? pass_tile(p, c->threads) : (dtype_size(dtype) == 2 ? 2048 : 1024);
+      p.tile = dtype_size(dtype) == 2 ? 2048 : 1024;
+    for (int s = 0; s < p.nsteps; ++s)  // dynamic tiles: one fold pass of each step's widest fold
+      p.steps[s].tile = (!p.nosync && c->tile < 0 && c->dyn_tiles) ? pass_tile(p, s, c->threads) : 0;
     p.dyn = (!p.nosync && p.tile > 0) ? c->dyn_tiles : 0;
     int segs = 0;
     for (int s = 0; s < p.nsteps; ++s) segs += p.steps[s].nseg;

@@ -555,15 +555,16 @@ __device__ __forceinline__ void run_step_work(const Plan& P, const Step& st, int
       ++k;
     }
   };
-  if (P.tile <= 0) {
+  const int64_t step_tile = st.tile > 0 ? st.tile : P.tile;
+  if (step_tile <= 0) {
     const int64_t my0 = T_vec * b / nb, my1 = T_vec * (b + 1) / nb;
     if (my0 < my1) body(my0, my1);
-  } else if (tile_ctr && (T_vec + P.tile - 1) / P.tile > nb) {
+  } else if (tile_ctr && (T_vec + step_tile - 1) / step_tile > nb) {
     // Dynamic tiles: CTA b starts with tile b, then claims tiles nb, nb+1, ...
     // from this step's counter.  The claim for the next tile is issued before
     // the current tile's loads, so its latency hides under them; CTAs that
     // get more NVLink bandwidth simply take more tiles (no fixed tail).
-    const int64_t tile = P.tile;
+    const int64_t tile = step_tile;
     const int64_t ntiles = (T_vec + tile - 1) / tile;
     int64_t t = b;
     while (t < ntiles) {
@@ -577,7 +578,7 @@ __device__ __forceinline__ void run_step_work(const Plan& P, const Step& st, int
       t = *s_next;
     }
   } else {
-    const int64_t tile = P.tile;
+    const int64_t tile = step_tile;
     for (int64_t t = b; t * tile < T_vec; t += nb) {
       const int64_t lo = t * tile;
       body(lo, lo + tile < T_vec ? lo + tile : T_vec);

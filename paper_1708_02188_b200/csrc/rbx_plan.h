@@ -71,6 +71,7 @@ struct Step {
   int32_t seg0, nseg;
   int32_t wait0, nwait;
   int32_t sig0, nsig;      // signals go to slot (step index + 1) of each listed peer
+  int32_t tile, pad_;      // work tile of this step in vectors (0: the plan's tile)
   int64_t total_vec;
 };
 
