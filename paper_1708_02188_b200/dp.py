@@ -50,6 +50,43 @@ def ddp_bucket_assignment(sizes_bytes, first_cap: int = 1 << 20, cap: int = 25 <
     return buckets
 
 
+class BucketTracker:
+    """Which buckets may be launched as gradients become ready (host logic of
+    one backward pass, CPU-testable).  Buckets launch strictly in index order
+    -- every rank must issue the same launch sequence, because launches of a
+    communicator pair up by epoch -- each exactly once, and only when all of
+    its parameters are ready; `finish()` releases the rest (parameters that
+    got no gradient this pass)."""
+
+    def __init__(self, bucket_sizes):
+        self.sizes = list(bucket_sizes)
+        self.active = False
+        self._pending = []
+        self._next = 0
+
+    def start(self) -> None:
+        self.active = True
+        self._pending = list(self.sizes)
+        self._next = 0
+
+    def ready(self, k: int) -> list:
+        """One parameter of bucket k is ready; returns the buckets to launch now."""
+        if self._pending[k] <= 0:
+            raise RuntimeError(f"bucket {k}: more gradients than parameters in one backward pass")
+        self._pending[k] -= 1
+        out = []
+        while self._next < len(self.sizes) and self._pending[self._next] == 0:
+            out.append(self._next)
+            self._next += 1
+        return out
+
+    def finish(self) -> list:
+        out = list(range(self._next, len(self.sizes)))
+        self._next = len(self.sizes)
+        self.active = False
+        return out
+
+
 class MultiringDataParallel:
     def __init__(self, module, ctx=None, comm: str = "multiring", group=None, bucket_cap_mb: float = 25.0,
                  first_bucket_mb: float = 1.0, average: bool = True, mode: str | None = None):
@@ -96,10 +133,8 @@ class MultiringDataParallel:
             self.ranges.append((lo, off))
         self.stream = torch.cuda.Stream(device=dev)
         self._launch_args = {}
-        self._armed = False
+        self._tracker = BucketTracker([len(b) for b in self.buckets])
         self._sync = True
-        self._pending = []
-        self._next = 0
         self.launched = 0
         self._hooks = [p.register_post_accumulate_grad_hook(self._on_grad) for p in self.params]
 
@@ -128,28 +163,21 @@ class MultiringDataParallel:
 
         if not self._sync:
             return
-        if not self._armed:
-            self._armed = True
-            self._pending = [len(b) for b in self.buckets]
-            self._next = 0
+        if not self._tracker.active:
+            self._tracker.start()
             torch.autograd.Variable._execution_engine.queue_callback(self._finish)
         if p.grad is None or p.grad.data_ptr() != self._ptr[id(p)]:
             raise RuntimeError("a parameter's .grad is no longer a view of the gradient arena "
                                "(zero_grad(set_to_none=True)?); use MultiringDataParallel.zero_grad()")
-        k = self._bucket_of[id(p)]
-        self._pending[k] -= 1
-        while self._next < len(self.buckets) and self._pending[self._next] == 0:
-            self._launch(self._next)
-            self._next += 1
+        for k in self._tracker.ready(self._bucket_of[id(p)]):
+            self._launch(k)
 
     def _finish(self) -> None:
         import torch
 
-        while self._next < len(self.buckets):  # parameters that got no gradient this step
-            self._launch(self._next)
-            self._next += 1
+        for k in self._tracker.finish():  # parameters that got no gradient this step
+            self._launch(k)
         torch.cuda.current_stream(self.device).wait_stream(self.stream)
-        self._armed = False
 
     def _launch(self, k: int) -> None:
         import torch

@@ -25,3 +25,42 @@ def test_resnet_buckets_match_ddp(name, want):
     order = list(reversed(list(m.parameters())))
     got = [sum(order[i].numel() for i in b) for b in ddp_bucket_assignment([p.numel() * 4 for p in order])]
     assert got == want
+
+
+def test_bucket_tracker_launch_order():
+    """Any readiness order: every bucket launches once, in index order, never
+    before all its parameters are ready; finish() releases the rest."""
+    import random
+
+    from paper_1708_02188_b200.dp import BucketTracker
+
+    rng = random.Random(0)
+    for _ in range(200):
+        sizes = [rng.randint(1, 5) for _ in range(rng.randint(1, 8))]
+        tr = BucketTracker(sizes)
+        tr.start()
+        events = [k for k, n in enumerate(sizes) for _ in range(n)]
+        rng.shuffle(events)
+        skip = rng.random() < 0.3  # some parameters get no gradient this pass
+        if skip:
+            events = events[: rng.randint(0, len(events))]
+        seen = [0] * len(sizes)
+        launched = []
+        for k in events:
+            seen[k] += 1
+            for b in tr.ready(k):
+                assert seen[b] == sizes[b], "launched before all its gradients were ready"
+                launched.append(b)
+        launched += tr.finish()
+        assert launched == list(range(len(sizes)))
+        assert not tr.active
+
+
+def test_bucket_tracker_rejects_double_gradients():
+    from paper_1708_02188_b200.dp import BucketTracker
+
+    tr = BucketTracker([1, 1])
+    tr.start()
+    assert tr.ready(1) == []
+    with pytest.raises(RuntimeError):
+        tr.ready(1)
