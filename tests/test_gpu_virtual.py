@@ -269,19 +269,23 @@ def test_ll_limits_and_large_ragged_inputs():
         vr.close()
 
 
-@pytest.mark.parametrize("mode", ["local", "fused", "push", "ll"])
-def test_cuda_graph_replay(mode):
-    """Epochs live in device memory, so a captured launch replays correctly
-    (CUDA graphs instead of per-call launches for static buffers)."""
+@pytest.mark.parametrize("mode,length,nblocks", [
+    ("local", 50_001, 4), ("fused", 50_001, 4), ("push", 50_001, 4), ("ll", 50_001, 4),
+    # more work tiles than CTAs: the dynamic-tile path (claim counters rewound at exit)
+    ("fused", 400_003, 2), ("ring_dims", 400_003, 2), ("push", 400_003, 2),
+])
+def test_cuda_graph_replay(mode, length, nblocks):
+    """Epochs and dynamic-tile counters live in device memory and are advanced /
+    rewound by the kernel itself, so a captured launch replays correctly (CUDA
+    graphs instead of per-call launches for static buffers)."""
     torch = _torch()
     from paper_1708_02188_b200.virtual import VirtualRanks
 
     dims = (2, 2, 2)
     grid = orc.Grid(dims)
-    length = 50_001
     parts = [orc.generate_input(4, 0, r, length, "f32") for r in range(8)]
     want = orc.closed_form_allreduce(grid, parts)
-    vr = VirtualRanks(dims, nblocks_per_rank=0 if mode == "local" else 4)
+    vr = VirtualRanks(dims, nblocks_per_rank=0 if mode == "local" else nblocks)
     src = [torch.from_numpy(p.copy()).cuda() for p in parts]
     ts = [s.clone() for s in src]
     s = torch.cuda.Stream()
