@@ -564,14 +564,22 @@ __device__ __forceinline__ void run_step_work(const Plan& P, const Step& st, int
     // from this step's counter.  The claim for the next tile is issued before
     // the current tile's loads, so its latency hides under them; CTAs that
     // get more NVLink bandwidth simply take more tiles (no fixed tail).
+    // With tail_split > 1 the last nb tiles' worth of vectors is cut into smaller
+    // tiles, so the CTAs finish the step within a small tile of each other.
     const int64_t tile = step_tile;
-    const int64_t ntiles = (T_vec + tile - 1) / tile;
+    const int64_t split = P.tail_split > 1 ? P.tail_split : 1;
+    const int64_t small = tile / split > 0 ? tile / split : 1;
+    const int64_t nbig = split > 1 ? (T_vec > (int64_t)nb * tile ? (T_vec - (int64_t)nb * tile) / tile : 0)
+                                   : (T_vec + tile - 1) / tile;
+    const int64_t big_end = nbig * tile;
+    const int64_t ntiles = nbig + (split > 1 ? (T_vec - big_end + small - 1) / small : 0);
     int64_t t = b;
     while (t < ntiles) {
       unsigned int nxt = 0;
       if (threadIdx.x == 0) nxt = (unsigned)nb + atomicAdd(tile_ctr, 1u);
-      const int64_t lo = t * tile;
-      body(lo, lo + tile < T_vec ? lo + tile : T_vec);
+      const int64_t lo = t < nbig ? t * tile : big_end + (t - nbig) * small;
+      const int64_t len = t < nbig ? tile : small;
+      body(lo, lo + len < T_vec ? lo + len : T_vec);
       __syncthreads();  // every thread has read *s_next for this tile
       if (threadIdx.x == 0) *s_next = (int)nxt;
       __syncthreads();
