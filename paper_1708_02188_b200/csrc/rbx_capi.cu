@@ -16,6 +16,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -118,7 +119,7 @@ struct rbx_comm {
   rbx::Geometry geo;
   uint32_t* sig_local = nullptr;     // own signal area(s)
   std::vector<uint32_t*> sig;        // per rank, mapped
-  std::vector<void*> opened_sig;
+  std::vector<void*> opened;  // base pointers of every IPC mapping this communicator opened (one ref each)
   rbx::ErrRecord* err_host = nullptr;
   rbx::ErrRecord* err_dev = nullptr;
   uint64_t timeout_ns = 30ull * 1000000000ull;  // runtime.py:39 DEFAULT_TIMEOUT_S
@@ -170,18 +171,28 @@ struct rbx_comm {
 
 namespace {
 
+// IPC mappings are per process (cudaIpcOpenMemHandle fails on a second open of
+// the same handle), so they are shared by every communicator of the process and
+// reference-counted.  ctypes releases the GIL, so calls may come from several
+// threads at once: the table has a lock.
 std::map<std::string, OpenedHandle>& opened_handles() {
   static std::map<std::string, OpenedHandle> m;
   return m;
 }
+std::mutex& opened_lock() {
+  static std::mutex mu;
+  return mu;
+}
 
-int open_handle(const rbx_ipc_handle_t& h, void** out) {
+int open_handle(rbx_comm* c, const rbx_ipc_handle_t& h, void** out) {
   std::string key(reinterpret_cast<const char*>(h.bytes), sizeof(h.bytes));
+  std::lock_guard<std::mutex> lock(opened_lock());
   auto& m = opened_handles();
   auto it = m.find(key);
   if (it != m.end()) {
     it->second.refs++;
     *out = it->second.ptr;
+    c->opened.push_back(it->second.ptr);
     return RBX_OK;
   }
   cudaIpcMemHandle_t ch;
@@ -190,7 +201,25 @@ int open_handle(const rbx_ipc_handle_t& h, void** out) {
   RBX_CUDA(cudaIpcOpenMemHandle(&p, ch, cudaIpcMemLazyEnablePeerAccess));
   m[key] = OpenedHandle{p, 1};
   *out = p;
+  c->opened.push_back(p);
   return RBX_OK;
+}
+
+// Drop this communicator's references; unmap what no communicator uses any more.
+void close_handles(rbx_comm* c) {
+  std::lock_guard<std::mutex> lock(opened_lock());
+  auto& m = opened_handles();
+  for (void* p : c->opened) {
+    for (auto it = m.begin(); it != m.end(); ++it) {
+      if (it->second.ptr != p) continue;
+      if (--it->second.refs <= 0) {
+        cudaIpcCloseMemHandle(p);
+        m.erase(it);
+      }
+      break;
+    }
+  }
+  c->opened.clear();
 }
 
 const void* kernel_for(int dtype) {
@@ -849,11 +878,10 @@ int rbx_comm_connect(rbx_comm_t* c, const rbx_ipc_handle_t* handles) {
   for (int q = 0; q < c->nranks; ++q) {
     if (q == c->rank) continue;
     void* p = nullptr;
-    int rc = open_handle(handles[q], &p);
+    int rc = open_handle(c, handles[q], &p);
     if (rc) return rc;
     c->sig[q] = static_cast<uint32_t*>(p);
     c->ll_at[q] = ll_area_of(c->sig[q]);
-    c->opened_sig.push_back(p);
   }
   c->connected = true;
   return RBX_OK;
@@ -867,21 +895,9 @@ int rbx_comm_destroy(rbx_comm_t* c) {
     cudaFree(kv.second.dev);
     cudaFree(kv.second.ptrs);
   }
-  auto& m = opened_handles();
-  for (auto it = m.begin(); it != m.end();) {
-    bool mine = false;
-    for (void* p : c->opened_sig) mine |= (p == it->second.ptr);
-    for (auto& b : c->bufs)
-      for (int q = 0; q < (int)b.at.size(); ++q)
-        if (q != c->rank && b.at[q] - 0 == it->second.ptr) mine = true;
-    if (mine && --it->second.refs <= 0) {
-      cudaIpcCloseMemHandle(it->second.ptr);
-      it = m.erase(it);
-    } else {
-      ++it;
-    }
-  }
+  close_handles(c);
   if (c->sig_local) cudaFree(c->sig_local);
+  if (c->trace_dev) cudaFree(c->trace_dev);
   if (c->order_ev) cudaEventDestroy(c->order_ev);
   if (c->inbox_owned && c->inbox_local) cudaFree(c->inbox_local);
   if (c->err_host) cudaFreeHost(c->err_host);
@@ -937,7 +953,7 @@ int rbx_set_inbox(rbx_comm_t* c, void* ptr, size_t bytes, const rbx_ipc_handle_t
       continue;
     }
     void* p = nullptr;
-    int rc = open_handle(handles[q], &p);
+    int rc = open_handle(c, handles[q], &p);
     if (rc) return rc;
     at[q] = static_cast<char*>(p) + offsets[q];
   }
@@ -971,7 +987,7 @@ int rbx_register_buffer(rbx_comm_t* c, void* ptr, size_t bytes, const rbx_ipc_ha
       continue;
     }
     void* p = nullptr;
-    int rc = open_handle(handles[q], &p);
+    int rc = open_handle(c, handles[q], &p);
     if (rc) return rc;
     b.at[q] = static_cast<char*>(p) + offsets[q];
   }
