@@ -136,7 +136,8 @@ struct rbx_comm {
   // dynamic work tiles (claimed from a per-step counter); env RBX_DYN.  With 2048-vector tiles
   // N=2 581 -> 595 GB/s, N=4 578 -> 597 GB/s busbw at 102.4 MB fp32 (profiles/r01_dyn_tiles_4gpu.txt)
   int dyn_tiles = 1;
-  int tail_split = 1;  // env RBX_TAIL_SPLIT: finer tiles for the last nb tiles' worth of a step
+  int tail_split = 1;
+  int fence_every = 0;  // env RBX_FENCE_EVERY: fence.sys every this many dynamic tiles (experiment)  // env RBX_TAIL_SPLIT: finer tiles for the last nb tiles' worth of a step
   int local_tile = 2048;   // same for the HBM-bound local mode (measured best of 0/512/2048/4096/8192/32768); env RBX_LOCAL_TILE
   size_t bytes_per_cta = 32 * 1024;   // adaptive CTA count per call; env RBX_BYTES_PER_CTA
   int min_blocks = 16;                // env RBX_MIN_BLOCKS
@@ -324,6 +325,7 @@ int common_init(rbx_comm* c, const int* dims, int ndims, int device, int threads
   if (const char* t = std::getenv("RBX_LOCAL_TILE")) c->local_tile = std::atoi(t);
   if (const char* t = std::getenv("RBX_DYN")) c->dyn_tiles = std::atoi(t);
   if (const char* t = std::getenv("RBX_TAIL_SPLIT")) c->tail_split = std::max(1, std::atoi(t));
+  if (const char* t = std::getenv("RBX_FENCE_EVERY")) c->fence_every = std::max(0, std::atoi(t));
   if (const char* t = std::getenv("RBX_LOCAL_GENERIC")) c->local_specialised = std::atoi(t) == 0;
   if (const char* t = std::getenv("RBX_LOCAL_CTAS_PER_SM")) c->local_ctas_per_sm = std::atoi(t);
   if (const char* t = std::getenv("RBX_BYTES_PER_CTA")) c->bytes_per_cta = (size_t)std::max(1L, std::atol(t));
@@ -408,6 +410,7 @@ int upload(rbx_comm* c, std::vector<rbx::Plan>& host, const std::vector<std::vec
       p.steps[s].tile = (!p.nosync && c->tile < 0 && c->dyn_tiles) ? pass_tile(p, s, c->threads) : 0;
     p.dyn = (!p.nosync && p.tile > 0) ? c->dyn_tiles : 0;
     p.tail_split = c->tail_split;
+    p.fence_every = c->fence_every;
     int segs = 0;
     for (int s = 0; s < p.nsteps; ++s) segs += p.steps[s].nseg;
     if (segs > maxsegs) maxsegs = segs;

@@ -574,12 +574,14 @@ __device__ __forceinline__ void run_step_work(const Plan& P, const Step& st, int
     const int64_t big_end = nbig * tile;
     const int64_t ntiles = nbig + (split > 1 ? (T_vec - big_end + small - 1) / small : 0);
     int64_t t = b;
+    int done_tiles = 0;
     while (t < ntiles) {
       unsigned int nxt = 0;
       if (threadIdx.x == 0) nxt = (unsigned)nb + atomicAdd(tile_ctr, 1u);
       const int64_t lo = t < nbig ? t * tile : big_end + (t - nbig) * small;
       const int64_t len = t < nbig ? tile : small;
       body(lo, lo + len < T_vec ? lo + len : T_vec);
+      if (P.fence_every > 0 && ++done_tiles % P.fence_every == 0) __threadfence_system();
       __syncthreads();  // every thread has read *s_next for this tile
       if (threadIdx.x == 0) *s_next = (int)nxt;
       __syncthreads();

@@ -82,6 +82,7 @@ struct alignas(16) Plan {  // 16-byte multiple: plans[v] is staged with int4 loa
   int32_t nblocks, tile;   // tile: vectors per round-robin work tile (0 = one contiguous range per CTA)
   int32_t dyn;             // after its first tile a CTA claims the next tile from a per-step counter
   int32_t tail_split;      // dyn: the last nb tiles' worth of a step is cut into tiles this many times smaller
+  int32_t fence_every, pad2_;  // dyn: fence.sys after every this many tiles (bounds writes in flight; 0 = never)
   uint8_t entry_peers[RBX_MAX_RANKS];
   uint32_t* sig[RBX_MAX_RANKS];   // signal area of every rank (mapped)
   uint32_t* my_sig;               // == sig[me]
