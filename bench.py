@@ -484,6 +484,13 @@ def main_multi(args):
     dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     t_e2e = e2e_t.mean().item() / 1e3
     ctx.check()
+    # the host result of the last e2e step must equal the device path's allreduce (all ranks)
+    restore()
+    ctx.collective("allreduce", work)
+    ctx.synchronize()
+    ok = torch.tensor([1 if torch.equal(out, work.cpu()) else 0], device=dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    e2e_ok = bool(ok.item())
 
     # the metric's "vs msg size" curve: the same timing (L2 flushed, device barrier,
     # one collective between events, max over ranks) on views of one large buffer
@@ -559,7 +566,7 @@ def main_multi(args):
             "cpu_baseline": None,
             "e2e": {"value": round(busbw(world, nbytes, t_e2e) * world, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": round(t_e2e * 1e3, 3),
-                    "chunks": args.e2e_chunks},
+                    "chunks": args.e2e_chunks, "result_matches_device_path": e2e_ok},
             "gpu_launches": launches,
             "clocks": clocks,
         }
