@@ -37,18 +37,19 @@ def _rank_main(rank, world, port, cases, q):
     from paper_1708_02188_b200.runtime import PlacedBuffer, RankContext, allgather, allreduce, reduce_scatter
 
     os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
-    torch.cuda.set_device(rank)
+    dev = rank % torch.cuda.device_count()  # > 1 rank per GPU when the box has fewer GPUs than ranks
+    torch.cuda.set_device(dev)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     out = []
     try:
         for case in cases:
             dims, mode, dtype, lengths, seed = case["dims"], case["mode"], case["dtype"], case["lengths"], case["seed"]
-            ctx = RankContext(rank, Grid(tuple(dims)), device=rank, mode=mode)
+            ctx = RankContext(rank, Grid(tuple(dims)), device=dev, mode=mode)
             for it, length in enumerate(lengths):
                 x = orc.generate_input(seed, it, rank, length, dtype)
                 t = ctx.empty(length, dtype)
                 t.copy_(torch.from_numpy(x))
-                buf = PlacedBuffer(t, device=f"cuda:{rank}")
+                buf = PlacedBuffer(t, device=f"cuda:{dev}")
                 op = case.get("op", "allreduce")
                 if op == "allreduce":
                     allreduce(ctx, buf)
@@ -95,8 +96,8 @@ def _dims_for(world):
 
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_all_decompositions_all_modes_bit_exact(world):
-    if cuda_count() < world:
-        pytest.skip(f"needs {world} GPUs")
+    if 2 * cuda_count() < world:  # up to 2 ranks per GPU (time-sliced contexts) below 8 GPUs
+        pytest.skip(f"needs {(world + 1) // 2} GPUs")
     g = golden("replay_digests")
     lengths = [0, 1, 17, 1000, 4099]
     cases = []
@@ -113,8 +114,8 @@ def test_all_decompositions_all_modes_bit_exact(world):
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_reference_runtime_digests_and_traffic(world):
     """Same inputs as the reference RUNTIME run (tests/golden/runtime_digests.json)."""
-    if cuda_count() < world:
-        pytest.skip(f"needs {world} GPUs")
+    if 2 * cuda_count() < world:  # up to 2 ranks per GPU (time-sliced contexts) below 8 GPUs
+        pytest.skip(f"needs {(world + 1) // 2} GPUs")
     g = golden("runtime_digests")
     grids = {2: [(2,)], 4: [(2, 2), (4,)], 8: [(2, 4), (2, 2, 2), (8,)]}[world]
     cases = [{"dims": d, "mode": "auto", "dtype": dt, "lengths": [0, 1, 17, 1000], "seed": world}
@@ -145,8 +146,8 @@ def test_reduce_scatter_allgather_pair(world):
 
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_full_size_config(world):
-    if cuda_count() < world:
-        pytest.skip(f"needs {world} GPUs")
+    if 2 * cuda_count() < world:  # up to 2 ranks per GPU (time-sliced contexts) below 8 GPUs
+        pytest.skip(f"needs {(world + 1) // 2} GPUs")
     n = 25_600_000
     cases = [{"dims": d, "mode": m, "dtype": "f32", "lengths": [n], "seed": 0}
              for d in ([(2, 4), (2, 2, 2)] if world == 8 else _dims_for(world)[:1]) for m in ("fused", "ring_dims", "push")]
