@@ -408,11 +408,19 @@ def main_multi(args):
     from paper_1708_02188_b200.runtime import RankContext, Workload, generate_input
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    # one rank per GPU; a box with fewer GPUs than ranks (a functional check of the
+    # N-rank path only, timings meaningless) shares GPUs and uses gloo for the host side
+    ngpu = torch.cuda.device_count()
+    local = int(os.environ.get("LOCAL_RANK", rank)) % ngpu
+    shared = world > ngpu
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     bind_host_to_gpu(local)
-    dist.init_process_group("nccl", device_id=dev)
+    if shared:
+        dist.init_process_group("gloo")
+        args.no_nccl = True
+    else:
+        dist.init_process_group("nccl", device_id=dev)
     dims = tuple(int(x) for x in args.dims.split("x")) if args.dims else DIMS_FOR.get(world, (world,))
     grid = Grid(dims)
     assert grid.size == world, f"dims {dims} do not match world size {world}"
@@ -549,7 +557,9 @@ def main_multi(args):
             "value": round(bw * world, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t * 1e3, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (reference generate_input, seed 0)",
-            "config": {"workload": workload_name(n, args.dtype, world, dims), "placement": f"{world} GPUs, one rank each",
+            "config": {"workload": workload_name(n, args.dtype, world, dims),
+                       "placement": (f"{world} ranks sharing {ngpu} GPUs (functional check only: timings are "
+                                     "not a measurement)") if shared else f"{world} GPUs, one rank each",
                        "ranks": world, "dims": list(dims), "bytes_per_rank": nbytes, "mode": args.mode,
                        "l2": "flushed between steps (256 MiB write per rank)",
                        "value_definition": "N * busbw, busbw = 2(N-1)/N*S/t (NCCL convention), max over ranks"},
