@@ -527,6 +527,27 @@ def main_multi(args):
         ctx.check()
         del big
 
+    # the reference's other two collectives on the same buffer (runtime.py:278-292):
+    # busbw = (N-1)/N * S / t each (NCCL convention for reduce-scatter / all-gather)
+    parts = {}
+    for op in ("reduce_scatter", "allgather"):
+        ts = []
+        for it in range(3 + 10):
+            restore()
+            ctx.barrier()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            ctx.collective(op, work)
+            e.record(stream)
+            torch.cuda.synchronize()
+            if it >= 3:
+                ts.append(s.elapsed_time(e))
+        tt = torch.tensor(ts, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        us = tt.median().item() * 1e3
+        parts[op] = {"us": round(us, 2), "busbw_gbs": round((world - 1) / world * nbytes / (us / 1e6) / 1e9, 2)}
+    ctx.check()
+
     nccl = None
     if not args.no_nccl:
         nbuf = pristine.clone()
@@ -573,6 +594,7 @@ def main_multi(args):
                          "algorithmic_bytes_per_launch": int(2 * (world - 1) / world * nbytes)},
             "nccl_busbw_gbs": nccl,
             "curve": curve or None,
+            "reduce_scatter": parts["reduce_scatter"], "allgather": parts["allgather"],
             "cpu_baseline": None,
             "e2e": {"value": round(busbw(world, nbytes, t_e2e) * world, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": round(t_e2e * 1e3, 3),
