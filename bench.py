@@ -20,7 +20,8 @@ restores the inputs and flushes L2 (256 MiB write, read back so no dirty
 lines are charged to the kernel) outside the timed region; the timed region
 is one allreduce, CUDA events on the launching stream, max over ranks.
 At N > 1 the line also carries `curve`: busbw at 4 KB, 64 KB, 1 MB, 16 MB,
-256 MB and 1 GiB per rank (the metric's "vs msg size"), timed the same way.
+256 MB and 1 GiB per rank (the metric's "vs msg size"), timed the same way, and
+`reduce_scatter` / `allgather` on the config buffer (busbw = (N-1)/N * S / t).
 `--impl reference` runs the reference runtime's phase loop ported to C
 (oracle/rbx_oracle.c, one thread per rank) on the host on the same job.
 """
