@@ -4,7 +4,7 @@ flags, entry/exit handshakes, 7-peer FUSED folds, LL -- when the sandbox only
 grants 4 GPUs.  Not a performance run (contexts on one GPU do not run
 concurrently, every handshake waits for a context switch).
 
-  torchrun --nproc-per-node 8 tools/oversub8.py
+  torchrun --nproc-per-node 8 tests/oversub8.py
 
 Checks every rank's result digest against the oracle's reference-order fold
 (test infrastructure, used only as the checker).  Prints one JSON line per case.

@@ -7,7 +7,7 @@ reference-order fold.  Meant to run under compute-sanitizer
 (memcheck / racecheck / synccheck / initcheck); on this sandbox's GPU pool the
 sanitizer is closed (tools/r72.sh shows the refusal), so it runs bare.
 
-  [compute-sanitizer --tool memcheck] python tools/sanitize.py [--modes local,fused,...]
+  [compute-sanitizer --tool memcheck] python tests/sanitize_workload.py [--modes local,fused,...]
 """
 
 import argparse

@@ -28,19 +28,22 @@ def main():
     args = ap.parse_args()
     import torch
 
-    from oracle import ringbox_oracle as orc
+    from paper_1708_02188_b200.runtime import Workload, generate_input
     from paper_1708_02188_b200.virtual import VirtualRanks
 
     n = args.elems
-    parts = [orc.generate_input(0, 0, r, n, "f32") for r in range(2)]
+    wl = Workload(lengths=(n,), dtype="f32", seed=0)
+    parts = [generate_input(wl, 0, r, n) for r in range(2)]
     bufs = [torch.from_numpy(parts[0]).to("cuda:0"), torch.from_numpy(parts[1]).to("cuda:1")]
     vr = VirtualRanks((2,), device=0, peer_devices=(1,))
     torch.cuda.set_device(0)
     vr.collective(bufs, mode="local")
     torch.cuda.synchronize(0)
     torch.cuda.synchronize(1)
-    want = orc.closed_form_allreduce(orc.Grid((2,)), parts)
-    ok = all(orc.sha256(b.cpu().numpy()) == orc.sha256(want) for b in bufs)
+    # grid (2,): every element is x0 + x1 (one IEEE add, commutative), so torch's
+    # add is the reference order here
+    want = torch.from_numpy(parts[0]) + torch.from_numpy(parts[1])
+    ok = all(torch.equal(b.cpu(), want) for b in bufs)
     stream = torch.cuda.current_stream(0)
     ts = []
     for _ in range(args.iters):
@@ -53,7 +56,7 @@ def main():
     t = statistics.median(ts)
     S = n * 4
     print(json.dumps({"harness": "grid (2,), one launch on cuda:0, rank-1 buffer on cuda:1 over NVLink",
-                      "bit_exact_vs_oracle": ok, "elems": n, "kernel_us": round(t * 1e6, 1),
+                      "bit_exact_vs_reference_order": ok, "elems": n, "kernel_us": round(t * 1e6, 1),
                       "nvlink_bytes_each_direction": S, "achieved_gbs_each_direction": round(S / t / 1e9, 1),
                       "pct_of_900": round(100 * S / t / 1e9 / 900, 1)}), flush=True)
 
