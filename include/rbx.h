@@ -101,6 +101,11 @@ int rbx_comm_connect(rbx_comm_t *comm, const rbx_ipc_handle_t *signal_handles);
 int rbx_comm_destroy(rbx_comm_t *comm);
 int rbx_comm_set_timeout(rbx_comm_t *comm, double seconds);
 int rbx_comm_info(rbx_comm_t *comm, int *rank, int *nranks, int *nblocks, int *threads, uint64_t *launches);
+/* Fault injection (the reference's Workload.crash_rank/crash_phase, runtime.py:393-394, 429-432): the
+ * NEXT collective launch of this communicator processes only `fraction` of its first data step (for
+ * MODE_LL: fraction > 0 = the scatter half) and then returns without signalling, as a rank that dies
+ * mid-collective with part of its data pushed.  The caller then exits; peers' watchdogs report it. */
+int rbx_comm_inject_fault(rbx_comm_t *comm, double fraction);
 /* Timeline of the last launch (RBX_TRACE=1 at create): %globaltimer ns of the first (words 0..31) and
  * last (32..63) CTA: 0 start, 1 plan staged, 2 entry signalled, 3+3s/4+3s/5+3s step s waited/worked/
  * signalled, 30 steps done, 31 exit.  Tracing / profiling subsystem. */

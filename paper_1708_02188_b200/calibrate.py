@@ -52,10 +52,15 @@ def measure(ctx, big_elems: int = 64 * 1024 * 1024, iters: int = 10) -> dict:
         n = ctx.grid.size
         bw.append(2 * (n - 1) / n * big_elems * 4 / t / 1e9)
     ctx.check()
-    vals = torch.tensor([lat, min(bw[2:])], device=dev, dtype=torch.float64)
+    # every rank must feed the planner the same numbers: the worst latency and the
+    # lowest median bandwidth over ranks
+    med_bw = sorted(bw[2:])[len(bw[2:]) // 2]
     if dist.is_available() and dist.is_initialized():
-        dist.all_reduce(vals, op=dist.ReduceOp.MAX)  # worst latency; (min over ranks via max of negatives below)
-    return {"latency_s": float(vals[0]), "bandwidth_gbps": float(sorted(bw[2:])[len(bw[2:]) // 2])}
+        from .exchange import allgather_objects
+
+        every = allgather_objects((lat, med_bw), ctx.group)
+        lat, med_bw = max(x[0] for x in every), min(x[1] for x in every)
+    return {"latency_s": float(lat), "bandwidth_gbps": float(med_bw)}
 
 
 def calibrated_topology(ctx, **kw):

@@ -168,6 +168,8 @@ struct rbx_comm {
   cudaEvent_t order_ev = nullptr;
   cudaStream_t last_stream = nullptr;
   bool has_last = false;
+  // one-shot fault injection for the next launch (rbx_comm_inject_fault); -1 = off
+  int fault_milli = -1;
 };
 
 namespace {
@@ -452,6 +454,8 @@ int launch(rbx_comm* c, const CachedPlan& cp, int dtype, cudaStream_t stream, bo
   a.err = c->err_dev;
   a.plan_bytes = cp.plan_bytes;
   a.trace = c->trace_dev;
+  a.fault_milli = c->fault_milli;
+  c->fault_milli = -1;
   void* params[] = {&a};
   dim3 grid((unsigned)(nblocks * cp.nplans)), block((unsigned)c->threads);
   const size_t smem = (size_t)((cp.plan_bytes + 15) / 16 * 16);
@@ -538,6 +542,8 @@ int ll_launch(rbx_comm* c, const std::vector<int>& ranks, void* const* bufs, siz
   }
   rbx::LLArgs* a = it->second.get();
   a->timeout_ns = c->timeout_ns;
+  a->fault = c->fault_milli < 0 ? -1 : (c->fault_milli == 0 ? 0 : 1);
+  c->fault_milli = -1;
   const int nb = a->nb;
   void* params[] = {a};
   rbx::LLArgsT<1> a1;  // per-rank form: the same fields with one hosted rank
@@ -914,6 +920,13 @@ int rbx_comm_set_timeout(rbx_comm_t* c, double seconds) {
   return RBX_OK;
 }
 
+int rbx_comm_inject_fault(rbx_comm_t* c, double fraction) {
+  if (!c) return fail(RBX_ERR_INVALID, "null communicator");
+  if (!(fraction >= 0.0 && fraction <= 1.0)) return fail(RBX_ERR_INVALID, "fault fraction must be in [0, 1]");
+  c->fault_milli = (int)(fraction * 1000.0 + 0.5);
+  return RBX_OK;
+}
+
 int rbx_comm_trace(rbx_comm_t* c, uint64_t* out, int cap) {
   if (!c) return fail(RBX_ERR_INVALID, "null communicator");
   if (!c->trace_dev) return fail(RBX_ERR_INVALID, "tracing is off (set RBX_TRACE=1 before creating the communicator)");
@@ -1026,6 +1039,7 @@ int rbx_allgather(rbx_comm_t* c, void* buf, size_t count, int dtype, int mode, v
 
 int rbx_allreduce_buckets(rbx_comm_t* c, void* const* bufs, const size_t* counts, int nbufs, int dtype, int mode,
                           void* stream) {
+  if (!c) return fail(RBX_ERR_INVALID, "null communicator");
   if (nbufs < 1) return fail(RBX_ERR_INVALID, "empty bucket list");
   if ((int64_t)nbufs * c->nranks > 4096) return fail(RBX_ERR_INVALID, "bucket list too long");
   return real_collective(c, bufs, counts, nbufs, dtype, RBX_OP_ALLREDUCE, mode, (cudaStream_t)stream);

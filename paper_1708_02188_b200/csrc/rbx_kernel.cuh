@@ -487,6 +487,10 @@ struct KernelArgs {
   uint64_t timeout_ns;
   ErrRecord* err;
   unsigned long long* trace;  // optional 64-word timeline (first/last CTA), or null
+  // fault injection (Workload.crash_phase, runtime.py:393-394, 429-432): -1 off; else the rank
+  // processes only the first fault_milli/1000 of its first data step's work tiles and its CTAs
+  // return without signalling -- a rank that dies with part of its data pushed
+  int fault_milli;
 };
 
 __device__ __forceinline__ bool flag_reached(uint32_t v, uint32_t e) { return (int32_t)(v - e) >= 0; }
@@ -519,7 +523,7 @@ __host__ __device__ constexpr size_t plan_smem_bytes(int nsegs) {
 template <typename T>
 __device__ __forceinline__ void run_step_work(const Plan& P, const Step& st, int b, int nb, SegCtx& s_seg,
                                               int& s_cur /* thread-local: same value in every thread */,
-                                              unsigned int* tile_ctr, int* s_next) {
+                                              unsigned int* tile_ctr, int* s_next, int fault_milli = -1) {
   const int64_t T_vec = st.total_vec;
   auto setup = [&](int k) {
     const Seg& sg = P.segs[st.seg0 + k];
@@ -556,9 +560,11 @@ __device__ __forceinline__ void run_step_work(const Plan& P, const Step& st, int
     }
   };
   const int64_t step_tile = st.tile > 0 ? st.tile : P.tile;
+  // injected fault: only the first fault_milli/1000 of the step's work units are processed
+  auto cut = [&](int64_t units) -> int64_t { return fault_milli < 0 ? units : units * fault_milli / 1000; };
   if (step_tile <= 0) {
     const int64_t my0 = T_vec * b / nb, my1 = T_vec * (b + 1) / nb;
-    if (my0 < my1) body(my0, my1);
+    if (my0 < my1 && b < cut(nb)) body(my0, my1);
   } else if (tile_ctr && (T_vec + step_tile - 1) / step_tile > nb) {
     // Dynamic tiles: CTA b starts with tile b, then claims tiles nb, nb+1, ...
     // from this step's counter.  The claim for the next tile is issued before
@@ -573,9 +579,10 @@ __device__ __forceinline__ void run_step_work(const Plan& P, const Step& st, int
                                    : (T_vec + tile - 1) / tile;
     const int64_t big_end = nbig * tile;
     const int64_t ntiles = nbig + (split > 1 ? (T_vec - big_end + small - 1) / small : 0);
+    const int64_t tlimit = cut(ntiles);
     int64_t t = b;
     int done_tiles = 0;
-    while (t < ntiles) {
+    while (t < tlimit) {
       unsigned int nxt = 0;
       if (threadIdx.x == 0) nxt = (unsigned)nb + atomicAdd(tile_ctr, 1u);
       const int64_t lo = t < nbig ? t * tile : big_end + (t - nbig) * small;
@@ -589,11 +596,13 @@ __device__ __forceinline__ void run_step_work(const Plan& P, const Step& st, int
     }
   } else {
     const int64_t tile = step_tile;
-    for (int64_t t = b; t * tile < T_vec; t += nb) {
+    const int64_t tlimit = cut((T_vec + tile - 1) / tile);
+    for (int64_t t = b; t * tile < T_vec && t < tlimit; t += nb) {
       const int64_t lo = t * tile;
       body(lo, lo + tile < T_vec ? lo + tile : T_vec);
     }
   }
+  if (fault_milli >= 0) return;  // a dying rank leaves its scalar edges undone
   for (int k = b % nb; k < st.nseg; k += nb) {  // scalar head/tail of segment k: CTA k mod nb
     const Seg& sg = P.segs[st.seg0 + k];
     if (sg.head + sg.tail == 0) continue;
@@ -696,7 +705,8 @@ __global__ void __launch_bounds__(512, 1) rbx_step_kernel(KernelArgs args) {
       int cur = -1;  // segment whose pointers are in s_seg (thread-local, uniform)
       unsigned int* ctr = (P.dyn && !P.nosync && P.tile > 0)
                               ? reinterpret_cast<unsigned int*>(my_sig + SigLayout::tiles_off + s) : nullptr;
-      run_step_work<T>(P, st, b, nb, s_seg, cur, ctr, &s_next);
+      run_step_work<T>(P, st, b, nb, s_seg, cur, ctr, &s_next, args.fault_milli);
+      if (args.fault_milli >= 0) return;  // injected crash: no signals, the epoch is not advanced
     }
     if (tr && s < 9) tr[4 + 3 * s] = global_ns();
     // ---- signal ----

@@ -72,6 +72,7 @@ struct LLArgsT {
   int nranks, nlev, nb;  // nb CTAs per rank
   int nhosted;           // ranks hosted by this launch
   int oneshot;           // 1: one-shot variant
+  int fault;             // fault injection (runtime.py:429-432): -1 off, 0 die at entry, 1 die after the scatter
   int64_t cap;           // words per slot
   uint64_t timeout_ns;
   ErrRecord* err;
@@ -153,8 +154,10 @@ struct LLWait {
   uint64_t t0, timeout_ns;
   volatile uint32_t* abort_word;
   bool failed;
-  // payload of the word at p once its epoch is current (0 on timeout/abort, failed set)
-  __device__ __forceinline__ uint32_t get(const unsigned long long* p) {
+  int peer;  // rank whose word timed out first (-1: the abort word was raised elsewhere)
+  // payload of the word at p (written by rank `from`) once its epoch is current
+  // (0 on timeout/abort, failed set)
+  __device__ __forceinline__ uint32_t get(const unsigned long long* p, int from) {
     uint32_t it = 0;
     while (true) {
       const unsigned long long v = ld_ll(p);
@@ -163,6 +166,7 @@ struct LLWait {
       if ((++it & 1023u) == 0) {
         if (*abort_word || global_ns() - t0 > timeout_ns) {
           failed = true;
+          if (!*abort_word) peer = from;
           return 0;
         }
       }
@@ -201,7 +205,7 @@ __device__ __forceinline__ void ll_fold_unit(const LLRank& R, const uint8_t* ord
       uint32_t w[WPU];
 #pragma unroll
       for (int j = 0; j < WPU; ++j)
-        w[j] = (uint32_t)(raw[k][j] >> 32) == e ? (uint32_t)raw[k][j] : wt.get(slot(p) + u * WPU + j);
+        w[j] = (uint32_t)(raw[k][j] >> 32) == e ? (uint32_t)raw[k][j] : wt.get(slot(p) + u * WPU + j, p);
       Acc x[LPU];
       F::lanes(w, x);
       f.feed(R.ctrl[k], x);
@@ -228,7 +232,7 @@ __global__ void __launch_bounds__(512, 1) rbx_ll_kernel(const __grid_constant__ 
   const int N = a.nranks, me = R.me;
   const int64_t cap = a.cap;
   __shared__ uint32_t s_epoch;
-  __shared__ int s_fail;
+  __shared__ int s_fail, s_peer;
   // timeline of thread 0 of the first and last CTA of the first hosted rank:
   // [0] start [1] epoch read [3] pushed [4] folded [5] gathered [30] done [31] exit
   unsigned long long* tr = nullptr;
@@ -240,9 +244,11 @@ __global__ void __launch_bounds__(512, 1) rbx_ll_kernel(const __grid_constant__ 
   if (threadIdx.x == 0) {
     s_epoch = *(volatile uint32_t*)(R.my_sig + SigLayout::epoch_off) + 1u;
     s_fail = 0;
+    s_peer = -1;
   }
   __syncthreads();
-  LLWait wt{s_epoch, global_ns(), a.timeout_ns, (volatile uint32_t*)(R.my_sig + SigLayout::abort_off), false};
+  if (a.fault == 0) return;  // injected crash before any data moved
+  LLWait wt{s_epoch, global_ns(), a.timeout_ns, (volatile uint32_t*)(R.my_sig + SigLayout::abort_off), false, -1};
   if (tr) tr[1] = global_ns();
   const uint32_t e = wt.e;
   const int64_t tid = (int64_t)b * blockDim.x + threadIdx.x, nthr = (int64_t)a.nb * blockDim.x;
@@ -265,6 +271,7 @@ __global__ void __launch_bounds__(512, 1) rbx_ll_kernel(const __grid_constant__ 
       }
     }
     if (tr) tr[3] = global_ns();
+    if (a.fault > 0) return;  // injected crash after the push
     const unsigned long long* slots = own + ll_oneshot_off(N) + par;
     for (int q = 0; q < N; ++q) {
       const int64_t o = R.off[q], len = R.len[q], nu = F::nunits(len);
@@ -300,6 +307,7 @@ __global__ void __launch_bounds__(512, 1) rbx_ll_kernel(const __grid_constant__ 
       }
     }
     if (tr) tr[3] = global_ns();
+    if (a.fault > 0) return;  // injected crash: my inputs are in the owners' slots, nothing else happens
     // 2. fold my region in the reference order; result -> my buffer + every peer's gather slot [me]
     {
       const int64_t o = R.off[me], len = R.len[me], nu = F::nunits(len);
@@ -333,7 +341,7 @@ __global__ void __launch_bounds__(512, 1) rbx_ll_kernel(const __grid_constant__ 
         for (int u = 0; u < U; ++u) {
           const int64_t w = w0 + u * nthr;
           if (w < nw) {
-            const uint32_t d = (uint32_t)(raw[u] >> 32) == e ? (uint32_t)raw[u] : wt.get(src + w);
+            const uint32_t d = (uint32_t)(raw[u] >> 32) == e ? (uint32_t)raw[u] : wt.get(src + w, q);
             if (!wt.failed) F::store(R.buf, o, len, w, d);
           }
         }
@@ -343,14 +351,17 @@ __global__ void __launch_bounds__(512, 1) rbx_ll_kernel(const __grid_constant__ 
   }
 
   if (tr) tr[30] = global_ns();
-  if (wt.failed) s_fail = 1;
+  if (wt.failed) {
+    s_fail = 1;
+    if (wt.peer >= 0) s_peer = wt.peer;
+  }
   __syncthreads();
   if (threadIdx.x != 0) return;
   if (s_fail) {
     if (atomicCAS(&a.err->code, 0, 3) == 0) {
       a.err->rank = me;
       a.err->step = 0;
-      a.err->peer = -1;
+      a.err->peer = s_peer;
     }
     *wt.abort_word = 1u;
     return;  // the epoch is not advanced: the communicator is in an error state

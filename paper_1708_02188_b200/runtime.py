@@ -409,6 +409,12 @@ class RankContext:
     def check(self) -> None:
         _native.check(self._L.rbx_check(self._comm))
 
+    def inject_fault(self, fraction: float) -> None:
+        """Arm a crash for the NEXT collective (Workload.crash_phase, runtime.py:429-432):
+        this rank moves only `fraction` of its data and returns without signalling,
+        so the peers' watchdogs see a rank that died mid-collective."""
+        _native.check(self._L.rbx_comm_inject_fault(self._comm, float(fraction)))
+
     def staging(self, n: int, dtype: str):
         key = (n, dtype)
         if key not in self._staging:
@@ -475,13 +481,22 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _worker(rank: int, ranks: int, dims: tuple, wl: dict, addr: tuple, timeout_s: float, q) -> None:
+def _crash_fraction(ctx: RankContext, length: int, crash_phase) -> float:
+    """The reference's dying rank runs `crash_phase` of its schedule's phases
+    (runtime.py:429-432); here it moves that fraction of its data."""
+    phases = len(ctx.schedule_for(length).phases) if length else 0
+    return min(1.0, (crash_phase or 0) / phases) if phases else 0.0
+
+
+def _worker(rank: int, ranks: int, dims: tuple, wl: dict, addr: tuple, timeout_s: float, q,
+            device: int | None = None) -> None:
     try:
         import torch
         import torch.distributed as dist
 
         os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = addr[0], str(addr[1])
-        torch.cuda.set_device(rank)
+        device = rank if device is None else device
+        torch.cuda.set_device(device)
         dist.init_process_group("gloo", rank=rank, world_size=ranks)
         workload = Workload(**wl)
         grid = build_grid(ranks, dims)
@@ -494,16 +509,24 @@ def _worker(rank: int, ranks: int, dims: tuple, wl: dict, addr: tuple, timeout_s
         except CollectiveError as exc:
             q.put(("error", rank, exc.rank, None, f"length mismatch: {exc}"))
             return
-        ctx = RankContext(rank, grid, device=rank, timeout_s=min(timeout_s, DEFAULT_TIMEOUT_S))
+        ctx = RankContext(rank, grid, device=device, timeout_s=min(timeout_s, DEFAULT_TIMEOUT_S))
         ctx.plan_hash = plan_fingerprint(dims, workload.dtype, lengths)
         times, digests = [], []
         for it, length in enumerate(lengths):
             data = generate_input(workload, it, rank, length)
-            buf = PlacedBuffer(torch.from_numpy(data).to(ctx.device), device=f"cuda:{rank}")
+            buf = PlacedBuffer(torch.from_numpy(data).to(ctx.device), device=f"cuda:{device}")
             if length:
                 ctx.register(buf.data)
             if workload.crash_rank == rank and it == 0:
-                os._exit(3)  # fault injection (runtime.py:393-394, 429-432)
+                # fault injection (runtime.py:393-394, 429-432): die in the middle of the first
+                # allreduce, after pushing `crash_phase` phases' worth of data
+                try:
+                    if length:
+                        ctx.inject_fault(_crash_fraction(ctx, length, workload.crash_phase))
+                        allreduce(ctx, buf)
+                        torch.cuda.synchronize()
+                finally:
+                    os._exit(3)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             allreduce(ctx, buf)
@@ -518,15 +541,18 @@ def _worker(rank: int, ranks: int, dims: tuple, wl: dict, addr: tuple, timeout_s
         q.put(("error", rank, rank, None, f"{type(exc).__name__}: {exc}"))
 
 
-def launch(ranks: int, plan, workload: Workload, rendezvous=None, timeout_s: float = DEFAULT_TIMEOUT_S) -> LaunchReport:
+def launch(ranks: int, plan, workload: Workload, rendezvous=None, timeout_s: float = DEFAULT_TIMEOUT_S, *,
+           share_gpus: bool = False) -> LaunchReport:
     """Spawn one process per GPU and run the workload's allreduces
-    (runtime.py:435-589).  Needs `ranks` visible CUDA devices."""
+    (runtime.py:435-589).  Needs `ranks` visible CUDA devices, unless
+    `share_gpus` places the ranks on the GPUs round-robin (time-sliced
+    contexts: correct, not fast -- for testing the N-rank path on a small box)."""
     dims = plan.grid.dims if isinstance(plan, Plan) else tuple(plan)
     build_grid(ranks, dims)
     report = LaunchReport(ranks=ranks, dims=dims)
     torch = _torch()
     ngpu = torch.cuda.device_count() if torch.cuda.is_available() else 0
-    if ngpu < ranks:
+    if ngpu < 1 or (ngpu < ranks and not share_gpus):
         report.error = f"launch needs {ranks} CUDA devices, found {ngpu} (no CPU fallback)"
         return report
     addr = rendezvous if rendezvous is not None else ("127.0.0.1", _free_port())
@@ -535,7 +561,7 @@ def launch(ranks: int, plan, workload: Workload, rendezvous=None, timeout_s: flo
     wl = dict(lengths=tuple(workload.lengths), dtype=workload.dtype, seed=workload.seed,
               crash_rank=workload.crash_rank, crash_phase=workload.crash_phase,
               length_overrides=dict(workload.length_overrides) if workload.length_overrides else None)
-    procs = {r: ctx.Process(target=_worker, args=(r, ranks, dims, wl, addr, timeout_s, q), daemon=True)
+    procs = {r: ctx.Process(target=_worker, args=(r, ranks, dims, wl, addr, timeout_s, q, r % ngpu), daemon=True)
              for r in range(ranks)}
     for p in procs.values():
         p.start()

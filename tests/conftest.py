@@ -44,3 +44,20 @@ def one_gpu():
 
 def need_gpus(n):
     return pytest.mark.skipif(cuda_count() < n, reason=f"needs {n} GPUs")
+
+
+def rank_device(rank: int) -> int:
+    """GPU of a rank process: one rank per GPU when the box has enough, else the
+    ranks share the GPUs round-robin (time-sliced contexts: every rank keeps its
+    own communicator, IPC mappings and flags, exactly as on a bigger box)."""
+    import torch
+
+    return rank % torch.cuda.device_count()
+
+
+def host_backend(world: int) -> str:
+    """torch.distributed backend for rank processes: NCCL refuses two ranks on
+    one GPU, so a box with fewer GPUs than ranks uses gloo for the host side."""
+    import torch
+
+    return "nccl" if world <= torch.cuda.device_count() else "gloo"

@@ -108,8 +108,8 @@ def _main(rank, world, port, scenario, q):
 def _run(world, scenario):
     import torch.multiprocessing as mp
 
-    if 2 * cuda_count() < world:
-        pytest.skip(f"needs {(world + 1) // 2} GPUs")
+    if cuda_count() < 1:
+        pytest.skip("no CUDA device")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()

@@ -4,14 +4,15 @@ bit-identical to the reference's allreduce of every bucket (oracle closed form
 over all ranks' local gradients, one allreduce per bucket as with
 Workload.lengths, runtime.py:390-398) times 1/N; the same step captured into a
 CUDA graph and replayed gives the same bits; NCCL through the same machinery
-agrees to rounding."""
+agrees to rounding.  Ranks share the GPUs round-robin on smaller boxes, with
+gloo (on CUDA tensors) standing in for NCCL as the comparison backend."""
 
 import os
 import socket
 
 import pytest
 
-from conftest import cuda_count
+from conftest import cuda_count, host_backend, rank_device
 
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
@@ -44,9 +45,14 @@ def _main(rank, world, port, q):
     from paper_1708_02188_b200.runtime import RankContext
 
     os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
-    torch.cuda.set_device(rank)
-    dev = torch.device("cuda", rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    d = rank_device(rank)
+    torch.cuda.set_device(d)
+    dev = torch.device("cuda", d)
+    backend = host_backend(world)  # gloo when ranks share a GPU (NCCL refuses that)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         gloo = dist.new_group(backend="gloo")
         torch.manual_seed(100 + rank)
@@ -63,7 +69,7 @@ def _main(rank, world, port, q):
         loss_of(plain).backward()
 
         dims = {2: (2,), 4: (2, 2)}[world]
-        ctx = RankContext(rank, Grid(dims), group=gloo, device=rank, blocking=False)
+        ctx = RankContext(rank, Grid(dims), group=gloo, device=d, blocking=False)
         model = _model(dev)
         dp = MultiringDataParallel(model, ctx, bucket_cap_mb=0.5, first_bucket_mb=0.25)
         nb = len(dp.buckets)
@@ -131,8 +137,8 @@ def _main(rank, world, port, q):
 
 @pytest.mark.parametrize("world", [2, 4])
 def test_dp_buckets_bit_exact_and_graph_replay(world):
-    if cuda_count() < world:
-        pytest.skip(f"needs {world} GPUs")
+    if cuda_count() < 1:
+        pytest.skip("no CUDA device")
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")

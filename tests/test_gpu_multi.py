@@ -1,5 +1,8 @@
-"""Multi-GPU parity: one process per GPU, NVLink-mapped peer buffers, real
-IPC handles (run with `gpurun --gpus 2|4`; skipped on a 1-GPU box).
+"""Multi-process parity: one process per rank, IPC-mapped peer buffers, real
+IPC handles.  On a box with N >= world GPUs every rank has its own GPU and the
+peer traffic crosses NVLink; with fewer GPUs the rank processes share them
+round-robin (conftest.rank_device), so the whole per-process path -- handle
+exchange, mappings, flags, watchdog -- runs on a 1-GPU box too.
 
 Mirrors the reference's runtime tests (pkg/tests/test_runtime.py:174-228,
 test_acceptance.py:41-73): digests equal the reference replay/runtime
@@ -13,7 +16,7 @@ import socket
 import numpy as np
 import pytest
 
-from conftest import cuda_count, golden
+from conftest import cuda_count, golden, rank_device
 from oracle import ringbox_oracle as orc
 
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
@@ -37,7 +40,7 @@ def _rank_main(rank, world, port, cases, q):
     from paper_1708_02188_b200.runtime import PlacedBuffer, RankContext, allgather, allreduce, reduce_scatter
 
     os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
-    dev = rank % torch.cuda.device_count()  # > 1 rank per GPU when the box has fewer GPUs than ranks
+    dev = rank_device(rank)
     torch.cuda.set_device(dev)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     out = []
@@ -96,8 +99,8 @@ def _dims_for(world):
 
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_all_decompositions_all_modes_bit_exact(world):
-    if 2 * cuda_count() < world:  # up to 2 ranks per GPU (time-sliced contexts) below 8 GPUs
-        pytest.skip(f"needs {(world + 1) // 2} GPUs")
+    if cuda_count() < 1:
+        pytest.skip("no CUDA device")
     g = golden("replay_digests")
     lengths = [0, 1, 17, 1000, 4099]
     cases = []
@@ -114,8 +117,8 @@ def test_all_decompositions_all_modes_bit_exact(world):
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_reference_runtime_digests_and_traffic(world):
     """Same inputs as the reference RUNTIME run (tests/golden/runtime_digests.json)."""
-    if 2 * cuda_count() < world:  # up to 2 ranks per GPU (time-sliced contexts) below 8 GPUs
-        pytest.skip(f"needs {(world + 1) // 2} GPUs")
+    if cuda_count() < 1:
+        pytest.skip("no CUDA device")
     g = golden("runtime_digests")
     grids = {2: [(2,)], 4: [(2, 2), (4,)], 8: [(2, 4), (2, 2, 2), (8,)]}[world]
     cases = [{"dims": d, "mode": "auto", "dtype": dt, "lengths": [0, 1, 17, 1000], "seed": world}
@@ -132,8 +135,8 @@ def test_reference_runtime_digests_and_traffic(world):
 
 @pytest.mark.parametrize("world", [2, 4])
 def test_reduce_scatter_allgather_pair(world):
-    if cuda_count() < world:
-        pytest.skip(f"needs {world} GPUs")
+    if cuda_count() < 1:
+        pytest.skip("no CUDA device")
     cases = [{"dims": d, "mode": m, "dtype": "f32", "lengths": [10007, 1], "seed": 11, "op": "rs+ag"}
              for d in _dims_for(world) for m in ("fused", "ring_dims", "push")]
     res = _spawn(world, cases)
@@ -146,8 +149,8 @@ def test_reduce_scatter_allgather_pair(world):
 
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_full_size_config(world):
-    if 2 * cuda_count() < world:  # up to 2 ranks per GPU (time-sliced contexts) below 8 GPUs
-        pytest.skip(f"needs {(world + 1) // 2} GPUs")
+    if cuda_count() < 1:
+        pytest.skip("no CUDA device")
     n = 25_600_000
     cases = [{"dims": d, "mode": m, "dtype": "f32", "lengths": [n], "seed": 0}
              for d in ([(2, 4), (2, 2, 2)] if world == 8 else _dims_for(world)[:1]) for m in ("fused", "ring_dims", "push")]
@@ -171,11 +174,12 @@ def _bucket_main(rank, world, port, q):
     from paper_1708_02188_b200.runtime import RankContext
 
     os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
-    torch.cuda.set_device(rank)
+    dev = rank_device(rank)
+    torch.cuda.set_device(dev)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         sizes = [2049, 7875, 6563, 1, 0, 6965, 1098]
-        ctx = RankContext(rank, Grid((world,) if world < 4 else (2, world // 2)), device=rank)
+        ctx = RankContext(rank, Grid((world,) if world < 4 else (2, world // 2)), device=dev)
         flat = ctx.empty(sum(sizes), "f32")
         xs = [orc.generate_input(5, k, rank, s, "f32") for k, s in enumerate(sizes)]
         views, off = [], 0
@@ -197,8 +201,8 @@ def _bucket_main(rank, world, port, q):
 def test_bucket_list_one_launch(world):
     """Config 4 semantics: a bucket list reduced in ONE launch, each bucket
     chunked on its own exactly like a Workload.lengths entry."""
-    if cuda_count() < world:
-        pytest.skip(f"needs {world} GPUs")
+    if cuda_count() < 1:
+        pytest.skip("no CUDA device")
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
@@ -228,13 +232,14 @@ def _bf16_main(rank, world, port, q):
     from paper_1708_02188_b200.runtime import RankContext
 
     os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
-    torch.cuda.set_device(rank)
+    dev = rank_device(rank)
+    torch.cuda.set_device(dev)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         out = []
         dims = (2, world // 2) if world >= 4 else (world,)
         for mode in ("fused", "ring_dims", "push", "ll"):
-            ctx = RankContext(rank, Grid(dims), device=rank, mode=mode)
+            ctx = RankContext(rank, Grid(dims), device=dev, mode=mode)
             rng = np.random.default_rng(100 + rank)
             bits = orc.bf16_round(rng.standard_normal(30_011).astype(np.float32))
             t = ctx.empty(len(bits), "bf16")
@@ -253,8 +258,8 @@ def _bf16_main(rank, world, port, q):
 def test_bf16_all_modes_match_policy(world):
     """bf16 (fp32 accumulate, one RNE): FUSED, RING_DIMS (fp32 partial
     workspaces between stages) and PUSH all equal the oracle policy."""
-    if cuda_count() < world:
-        pytest.skip(f"needs {world} GPUs")
+    if cuda_count() < 1:
+        pytest.skip("no CUDA device")
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
@@ -285,15 +290,16 @@ def _calib_main(rank, world, port, q):
     from paper_1708_02188_b200.runtime import RankContext
 
     os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
-    torch.cuda.set_device(rank)
+    dev = rank_device(rank)
+    torch.cuda.set_device(dev)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        ctx = RankContext(rank, Grid((world,)), device=rank, blocking=False)
+        ctx = RankContext(rank, Grid((world,)), device=dev, blocking=False)
         t, m = calibrated_topology(ctx, big_elems=16 * 1024 * 1024, iters=4)
         p = plan(t, t.devices(), 0.1024)
         # errors surface as the reference's exception types
         errs = []
-        stray = torch.empty(1000, device=f"cuda:{rank}")
+        stray = torch.empty(1000, device=f"cuda:{dev}")
         try:
             import ctypes
 
@@ -313,8 +319,8 @@ def _calib_main(rank, world, port, q):
 def test_planner_calibration_and_abi_errors():
     """measured per-stage latency and bus bandwidth feed the
     reference planner through a B200 topology; unregistered buffers are refused."""
-    if cuda_count() < 2:
-        pytest.skip("needs 2 GPUs")
+    if cuda_count() < 1:
+        pytest.skip("no CUDA device")
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
@@ -326,9 +332,14 @@ def test_planner_calibration_and_abi_errors():
     res = sorted(q.get(timeout=600) for _ in range(2))
     for p in procs:
         p.join(timeout=60)
+    shared = cuda_count() < 2  # two time-sliced contexts on one GPU: a barrier costs a time slice
     for rank, status, m, dims, errs in res:
         assert status == "ok", m
-        assert 0 < m["latency_s"] < 1e-3 and m["bandwidth_gbps"] > 100
+        if shared:
+            assert m["latency_s"] > 0 and m["bandwidth_gbps"] > 0
+        else:
+            assert 0 < m["latency_s"] < 1e-3 and m["bandwidth_gbps"] > 100
+        assert m == res[0][2], "ranks must feed the planner the same calibration"
         assert dims == (2,)
         assert errs and errs[0].startswith("unregistered:buffer is not registered")
 
@@ -336,20 +347,20 @@ def test_planner_calibration_and_abi_errors():
 def test_launch_api_matches_reference_and_detects_faults():
     """`launch` (runtime.py:435-589): serial-oracle digests for i64, a crashed
     rank is attributed, a shape mismatch aborts."""
-    if cuda_count() < 2:
-        pytest.skip("needs 2 GPUs")
+    if cuda_count() < 1:
+        pytest.skip("no CUDA device")
     from paper_1708_02188_b200.runtime import Workload, generate_input, launch
 
-    n = 4 if cuda_count() >= 4 else 2
-    dims = (2, 2) if n == 4 else (2,)
+    n, dims = 4, (2, 2)
     w = Workload(lengths=(0, 1, 17, 64), seed=11)
-    rep = launch(n, dims, w)
+    rep = launch(n, dims, w, share_gpus=True)
     assert rep.ok, rep.error
     for it, length in enumerate(w.lengths):
         total = np.sum([generate_input(w, it, r, length) for r in range(n)], axis=0).astype(np.int64)
         want = hashlib.sha256(np.asarray(total, dtype=np.int64).tobytes()).hexdigest()
         assert {rep.results[r].digests[it] for r in range(n)} == {want}
-    rep = launch(2, (2,), Workload(lengths=(50,), seed=1, length_overrides={1: 49}))
+    rep = launch(2, (2,), Workload(lengths=(50,), seed=1, length_overrides={1: 49}), share_gpus=True)
     assert not rep.ok and "mismatch" in rep.error
-    rep = launch(n, (n,), Workload(lengths=(100,), seed=1, crash_rank=1, crash_phase=1), timeout_s=15)
+    rep = launch(n, (n,), Workload(lengths=(100,), seed=1, crash_rank=1, crash_phase=1), timeout_s=15,
+                 share_gpus=True)
     assert not rep.ok and rep.failed_rank == 1
