@@ -24,6 +24,7 @@
 #include "rbx_kernel.cuh"
 #include "rbx_plan.h"
 
+#include "rbx_fused.cuh"
 #include "rbx_local.cuh"
 #include "rbx_ll.cuh"
 
@@ -46,6 +47,12 @@ const void* ll_kernel_i64(int maxv);
 const void* ll_kernel_bf16(int maxv);
 const void* ll_kernel_f16(int maxv);
 const void* ll_kernel_i32(int maxv);
+const void* fused_kernel_f32(int nsrc, int nlev, int maxseg);
+const void* fused_kernel_f64(int nsrc, int nlev, int maxseg);
+const void* fused_kernel_i64(int nsrc, int nlev, int maxseg);
+const void* fused_kernel_bf16(int nsrc, int nlev, int maxseg);
+const void* fused_kernel_f16(int nsrc, int nlev, int maxseg);
+const void* fused_kernel_i32(int nsrc, int nlev, int maxseg);
 }  // namespace rbx
 
 namespace {
@@ -93,6 +100,11 @@ struct CachedPlan {
   const void* local_fn = nullptr;  // specialised MODE_LOCAL kernel (rbx_local.cuh), if the shape has one
   std::shared_ptr<rbx::LocalArgs> local_args;
   int local_grid = 0;
+  // specialised FUSED allreduce kernel (rbx_fused.cuh), if the shape has one: arguments for
+  // one segment (fused1) or a bucket list of up to RBX_FUSED_MAXSEG (fusedN)
+  const void* fused_fn = nullptr;
+  std::shared_ptr<rbx::FusedArgsT<1>> fused1;
+  std::shared_ptr<rbx::FusedArgsT<RBX_FUSED_MAXSEG>> fusedN;
 };
 
 struct LLKey {  // cached MODE_LL launch arguments: buffers, count, dtype
@@ -170,6 +182,10 @@ struct rbx_comm {
   bool has_last = false;
   // one-shot fault injection for the next launch (rbx_comm_inject_fault); -1 = off
   int fault_milli = -1;
+  // FUSED allreduce through the specialised kernel (rbx_fused.cuh) where the grid shape has one;
+  // env RBX_FUSED_KERNEL=0 forces the generic step interpreter
+  bool fused_specialised = true;
+  int pdl = 1;  // programmatic dependent launch for the fused kernel; env RBX_PDL
 };
 
 namespace {
@@ -257,6 +273,63 @@ unsigned long long* ll_area_of(uint32_t* sig) {
   return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(sig) + ll_offset());
 }
 
+const void* fused_kernel_for(int dtype, int nsrc, int nlev, int maxseg) {
+  switch (dtype) {
+    case RBX_F32: return rbx::fused_kernel_f32(nsrc, nlev, maxseg);
+    case RBX_F64: return rbx::fused_kernel_f64(nsrc, nlev, maxseg);
+    case RBX_I64: return rbx::fused_kernel_i64(nsrc, nlev, maxseg);
+    case RBX_BF16: return rbx::fused_kernel_bf16(nsrc, nlev, maxseg);
+    case RBX_F16: return rbx::fused_kernel_f16(nsrc, nlev, maxseg);
+    case RBX_I32: return rbx::fused_kernel_i32(nsrc, nlev, maxseg);
+    default: return nullptr;
+  }
+}
+
+// Arguments of the specialised FUSED kernel from a FUSED allreduce plan: step 0 folds
+// every segment from all N buffers and stores into all N, step 1 is the exit wait.
+template <int MAXSEG>
+bool fused_args_from_plan(const rbx_comm* c, const rbx::Plan& p, const std::vector<void*>& table, int threads,
+                          rbx::FusedArgsT<MAXSEG>* a) {
+  std::memset(a, 0, sizeof(*a));
+  const int N = c->nranks;
+  if (p.nsteps != 2 || p.steps[1].nseg != 0 || p.nentry != N - 1) return false;
+  const rbx::Step& st = p.steps[0];
+  if (st.nseg < 1 || st.nseg > MAXSEG) return false;
+  a->nseg = st.nseg;
+  a->me = c->rank;
+  a->npeers = N - 1;
+  a->total_vec = st.total_vec;
+  a->my_sig = c->sig[c->rank];
+  for (int i = 0, q = 0; q < N; ++q) {
+    if (q == c->rank) continue;
+    a->peer_rank[i] = (uint8_t)q;
+    a->peer_sig[i++] = c->sig[q];
+  }
+  const rbx::Seg& s0 = p.segs[st.seg0];
+  for (int j = 0; j < N; ++j) a->ctrl[j] = s0.ctrl[j];
+  int u = 0;
+  for (int k = 0; k < st.nseg; ++k) {
+    const rbx::Seg& sg = p.segs[st.seg0 + k];
+    if (sg.nsrc != N || sg.ndst != N || sg.acc || sg.nlev != s0.nlev) return false;
+    for (int j = 0; j < N; ++j)
+      if (sg.ctrl[j] != s0.ctrl[j]) return false;
+    rbx::FusedSeg& fs = a->seg[k];
+    fs.vec_begin = sg.vec_begin;
+    fs.nvec = sg.nvec;
+    fs.body_off = sg.body_off;
+    fs.off = sg.off;
+    fs.head = sg.head;
+    fs.tail = sg.tail;
+    for (int j = 0; j < N; ++j) {
+      fs.src[j] = static_cast<const char*>(table[sg.tbl + sg.src[j]]);
+      fs.dst[j] = static_cast<char*>(table[sg.tbl + sg.dst[j]]);
+    }
+  }
+  u = RBX_FUSED_LD / N > 0 ? RBX_FUSED_LD / N : 1;
+  a->tile = threads * u;
+  return true;
+}
+
 const void* local_kernel_for(int dtype, int v, int nlev) {
   switch (dtype) {
     case RBX_F32: return rbx::local_kernel_f32(v, nlev);
@@ -329,6 +402,8 @@ int common_init(rbx_comm* c, const int* dims, int ndims, int device, int threads
   if (const char* t = std::getenv("RBX_TAIL_SPLIT")) c->tail_split = std::max(1, std::atoi(t));
   if (const char* t = std::getenv("RBX_FENCE_EVERY")) c->fence_every = std::max(0, std::atoi(t));
   if (const char* t = std::getenv("RBX_LOCAL_GENERIC")) c->local_specialised = std::atoi(t) == 0;
+  if (const char* t = std::getenv("RBX_FUSED_KERNEL")) c->fused_specialised = std::atoi(t) != 0;
+  if (const char* t = std::getenv("RBX_PDL")) c->pdl = std::atoi(t) != 0;
   if (const char* t = std::getenv("RBX_LOCAL_CTAS_PER_SM")) c->local_ctas_per_sm = std::atoi(t);
   if (const char* t = std::getenv("RBX_BYTES_PER_CTA")) c->bytes_per_cta = (size_t)std::max(1L, std::atol(t));
   if (const char* t = std::getenv("RBX_MIN_BLOCKS")) c->min_blocks = std::max(1, std::atoi(t));
@@ -466,6 +541,42 @@ int launch(rbx_comm* c, const CachedPlan& cp, int dtype, cudaStream_t stream, bo
   } else {
     RBX_CUDA(cudaLaunchKernel(fn, grid, block, params, smem, stream));
   }
+  c->launches++;
+  return order_after(c, stream, capturing);
+}
+
+// Launch of the specialised FUSED kernel (rbx_fused.cuh) with programmatic
+// dependent launch: its CTAs may become resident while the previous kernel on
+// the stream drains (griddepcontrol.wait guards every memory read).
+int fused_launch(rbx_comm* c, CachedPlan& cp, cudaStream_t stream, int nb) {
+  void* argp;
+  if (cp.fused1) {
+    cp.fused1->timeout_ns = c->timeout_ns;
+    cp.fused1->trace = c->trace_dev;
+    cp.fused1->fault_milli = c->fault_milli;
+    argp = cp.fused1.get();
+  } else {
+    cp.fusedN->timeout_ns = c->timeout_ns;
+    cp.fusedN->trace = c->trace_dev;
+    cp.fusedN->fault_milli = c->fault_milli;
+    argp = cp.fusedN.get();
+  }
+  c->fault_milli = -1;
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)nb);
+  cfg.blockDim = dim3((unsigned)c->threads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = c->pdl;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* params[] = {argp};
+  bool capturing = false;
+  if (int rc = order_before(c, stream, &capturing)) return rc;
+  RBX_CUDA(cudaLaunchKernelExC(&cfg, cp.fused_fn, params));
   c->launches++;
   return order_after(c, stream, capturing);
 }
@@ -722,6 +833,27 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
     cp.uses_inbox = push || ws;
     int rc = upload(c, host, {ptrs}, &cp, dtype);
     if (rc) return rc;
+    const bool fused = (mode == RBX_MODE_FUSED || mode == RBX_MODE_AUTO) && op == RBX_OP_ALLREDUCE && !push && !ws;
+    if (fused && c->fused_specialised) {
+      const int nseg = host[0].nsteps ? host[0].steps[0].nseg : 0;
+      const int maxseg = nseg <= 1 ? 1 : RBX_FUSED_MAXSEG;
+      const void* fn = fused_kernel_for(dtype, c->nranks, (int)c->geo.active_dims().size(), maxseg);
+      int per_sm = 0;
+      if (fn) RBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, c->threads, 0));
+      if (fn && per_sm * c->sm_count >= c->nblocks) {
+        bool ok;
+        if (maxseg == 1) {
+          cp.fused1 = std::make_shared<rbx::FusedArgsT<1>>();
+          ok = fused_args_from_plan(c, host[0], ptrs, c->threads, cp.fused1.get());
+          if (!ok) cp.fused1.reset();
+        } else {
+          cp.fusedN = std::make_shared<rbx::FusedArgsT<RBX_FUSED_MAXSEG>>();
+          ok = fused_args_from_plan(c, host[0], ptrs, c->threads, cp.fusedN.get());
+          if (!ok) cp.fusedN.reset();
+        }
+        if (ok) cp.fused_fn = fn;
+      }
+    }
     it = c->plans.emplace(key, cp).first;
   }
   // CTAs per call: enough to cover the bytes (bandwidth), few for small
@@ -735,6 +867,7 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
     if (want < nb) nb = (int)(want < c->min_blocks ? c->min_blocks : want);
   }
   if (nb > c->nblocks) nb = c->nblocks;
+  if (it->second.fused_fn) return fused_launch(c, it->second, stream, nb);
   return launch(c, it->second, dtype, stream, false, nb);
 }
 

@@ -1,0 +1,15 @@
+// Instantiations of the specialised FUSED kernel (rbx_fused.cuh) for dtype bf16:
+// one TU per dtype so the builds run in parallel.
+#include "rbx_fused.cuh"
+
+namespace rbx {
+const void* fused_kernel_bf16(int nsrc, int nlev, int maxseg) {
+#define RBX_FUSED_CASE(N, L)                                                                          \
+  if (nsrc == N && nlev == L)                                                                         \
+    return maxseg == 1 ? reinterpret_cast<const void*>(&rbx_fused_kernel<__nv_bfloat16, N, L, 1>)                \
+                       : reinterpret_cast<const void*>(&rbx_fused_kernel<__nv_bfloat16, N, L, RBX_FUSED_MAXSEG>);
+  RBX_FUSED_SHAPES(RBX_FUSED_CASE)
+#undef RBX_FUSED_CASE
+  return nullptr;
+}
+}  // namespace rbx

@@ -364,3 +364,90 @@ def test_launch_api_matches_reference_and_detects_faults():
     rep = launch(n, (n,), Workload(lengths=(100,), seed=1, crash_rank=1, crash_phase=1), timeout_s=15,
                  share_gpus=True)
     assert not rep.ok and rep.failed_rank == 1
+
+
+def _edge_main(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1708_02188_b200.multiring import Grid
+    from paper_1708_02188_b200.runtime import RankContext
+
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dev = rank_device(rank)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = []
+    try:
+        for dims in _dims_for(world):
+            ctx = RankContext(rank, Grid(tuple(dims)), device=dev, mode="fused", nblocks=16)
+            for dtype, n in (("f32", 100_003), ("i64", 33_335), ("f64", 4099)):
+                x = orc.generate_input(21, 0, rank, n, dtype)
+                # (1) a view 1 element past a 16-byte boundary on every rank: scalar head/tail peel
+                base = ctx.empty(n + 3, dtype)
+                t = base[1:1 + n]
+                t.copy_(torch.from_numpy(x))
+                ctx.collective("allreduce", t)
+                out.append(("misaligned", tuple(dims), dtype, n, orc.sha256(t.cpu().numpy())))
+                # (2) three element windows compose to the full allreduce
+                w = ctx.empty(n, dtype)
+                w.copy_(torch.from_numpy(x))
+                for lo, hi in ((0, n // 3), (n // 3, n - 5), (n - 5, n)):
+                    ctx.allreduce_window(w, lo, hi)
+                out.append(("windows", tuple(dims), dtype, n, orc.sha256(w.cpu().numpy())))
+            # (3) a bucket list (one launch; the multi-segment form of the kernel)
+            sizes = [5000, 1, 0, 12_345, 777]
+            flat = ctx.empty(sum(sizes) + 1, "f32")
+            views, off = [], 1
+            for k, s in enumerate(sizes):
+                v = flat[off:off + s]
+                v.copy_(torch.from_numpy(orc.generate_input(22, k, rank, s, "f32")))
+                views.append(v)
+                off += s
+            l0 = ctx.launches
+            ctx.allreduce_buckets(views)
+            out.append(("buckets", tuple(dims), "f32", ctx.launches - l0,
+                        [orc.sha256(v.cpu().numpy()) for v in views]))
+            ctx.close()
+        q.put((rank, "ok", out))
+    except Exception:  # noqa: BLE001
+        import traceback
+
+        q.put((rank, "error", traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_fused_kernel_misaligned_windows_buckets(world):
+    """The specialised FUSED kernel (rbx_fused.cuh) on the per-rank path: views
+    whose element 0 is not 16-byte aligned (scalar edges), element windows
+    (rbx_allreduce_window) and a bucket list with empty and 1-element buckets,
+    every result equal to the reference-order fold bit for bit."""
+    if cuda_count() < 1:
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_edge_main, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=900) for _ in range(world)), key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+    for item in res:
+        assert item[1] == "ok", item[2]
+    sizes = [5000, 1, 0, 12_345, 777]
+    for rank, _, out in res:
+        for kind, dims, dtype, n, dig in out:
+            g = orc.Grid(dims)
+            if kind == "buckets":
+                assert n == 1, "bucket list must be one launch"
+                for k, s in enumerate(sizes):
+                    parts = [orc.generate_input(22, k, r, s, "f32") for r in range(world)]
+                    assert dig[k] == orc.sha256(orc.closed_form_allreduce(g, parts)), (rank, dims, k)
+            else:
+                parts = [orc.generate_input(21, 0, r, n, dtype) for r in range(world)]
+                assert dig == orc.sha256(orc.closed_form_allreduce(g, parts)), (rank, kind, dims, dtype)
