@@ -63,8 +63,8 @@ def parse_args():
     p.add_argument("--no-nccl", action="store_true")
     p.add_argument("--curve", type=int, default=1, help="N>1: add busbw at 4 KB..1 GiB to the line")
     p.add_argument("--e2e-chunks", type=int, default=None,
-                   help="pipeline windows for the host-buffer e2e leg (default 8 at N=1, 32 at N>1: "
-                        "best measured against the host PCIe ceiling, profiles/r01_pcie_probe_*gpu.jsonl)")
+                   help="N=1: pipeline windows of the host-buffer e2e leg (default 8, best measured against the "
+                        "host PCIe ceiling, profiles/r01_pcie_probe_*gpu.jsonl); N>1 uses the runtime's default")
     a = p.parse_args()
     if a.e2e_chunks is None:
         a.e2e_chunks = 8 if a.gpus == 1 else 32
@@ -140,43 +140,6 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
                 "samples": len(sm)}
-
-
-def pipelined_e2e(n, chunks, h2d, red, d2h, stream, iters, warmup, before):
-    """Time host->device->host steps: window k's H2D, reduction and D2H run on
-    three streams so PCIe in both directions overlaps the kernels.  Returns
-    per-step milliseconds (CUDA events on `stream`, which brackets the step)."""
-    import torch
-
-    s_in, s_red, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-    bounds = [(n * k // chunks, n * (k + 1) // chunks) for k in range(chunks)]
-    out = []
-    for it in range(iters):
-        before()
-        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        start.record(stream)
-        for st in (s_in, s_red, s_out):
-            st.wait_event(start)
-        for lo, hi in bounds:
-            with torch.cuda.stream(s_in):
-                h2d(lo, hi)
-            ev_in = torch.cuda.Event()
-            ev_in.record(s_in)
-            s_red.wait_event(ev_in)
-            red(lo, hi, s_red)
-            ev_red = torch.cuda.Event()
-            ev_red.record(s_red)
-            s_out.wait_event(ev_red)
-            with torch.cuda.stream(s_out):
-                d2h(lo, hi)
-        ev_done = torch.cuda.Event()
-        ev_done.record(s_out)
-        stream.wait_event(ev_done)
-        end.record(stream)
-        torch.cuda.synchronize()
-        if it >= warmup:
-            out.append(start.elapsed_time(end))
-    return out
 
 
 def bind_host_to_gpu(index: int) -> list:
@@ -278,6 +241,7 @@ def run_reference(args):
 
 def main_single(args):
     """N = 1: the 8 ranks of config 2 on one GPU, local-reduce kernel."""
+    import numpy as np
     import torch
 
     from paper_1708_02188_b200.runtime import Workload, generate_input
@@ -336,30 +300,28 @@ def main_single(args):
     nbytes = n * esz
     bw = busbw(ranks, nbytes, t)
 
-    # e2e through the C ABI with HOST buffers: pinned H2D of every rank's input,
-    # the collective, D2H of every rank's result -- all inside the timed region,
-    # pipelined over element windows on three streams (copy-in / reduce / copy-out).
-    pinned = [h.pin_memory() for h in host]
-    outs = [torch.empty_like(h).pin_memory() for h in host]
-
-    def h2d(lo, hi):
-        for w, h in zip(work, pinned):
-            w[lo:hi].copy_(h[lo:hi], non_blocking=True)
-
-    def d2h(lo, hi):
-        for o, w in zip(outs, work):
-            o[lo:hi].copy_(w[lo:hi], non_blocking=True)
-
-    def red(lo, hi, st):
-        vr.collective(work, mode="local", stream=st, window=(lo, hi))
-
-    e2e_ms = pipelined_e2e(n, args.e2e_chunks, h2d, red, d2h, stream, args.warmup + max(3, min(args.steps, 10)),
-                           args.warmup, lambda: flush_l2(scratch))
-    t_e2e = statistics.mean(e2e_ms) / 1e3
-    restore()
-    vr.collective(work, mode="local")
-    torch.cuda.synchronize()
-    e2e_ok = all(torch.equal(o, w.cpu()) for o, w in zip(outs[:2], work[:2]))
+    # e2e through the product API with HOST buffers (VirtualRanks.allreduce_host: the
+    # numpy arrays page-locked once, H2D / kernel / D2H of element windows overlapped
+    # on three streams) -- every byte crosses PCIe both ways inside the timed region
+    e2e_ms, e2e_ok = [], False
+    if args.dtype == "f32":
+        arrays = [h.numpy().copy() for h in host]
+        for it in range(args.warmup + max(3, min(args.steps, 10))):
+            for a, h in zip(arrays, host):
+                a[...] = h.numpy()
+            flush_l2(scratch)
+            s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s_ev.record(stream)
+            vr.allreduce_host(arrays, mode="local", windows=args.e2e_chunks)
+            e_ev.record(stream)
+            torch.cuda.synchronize()
+            if it >= args.warmup:
+                e2e_ms.append(s_ev.elapsed_time(e_ev))
+        restore()
+        vr.collective(work, mode="local")
+        torch.cuda.synchronize()
+        e2e_ok = all(np.array_equal(a, w.cpu().numpy()) for a, w in zip(arrays[:2], work[:2]))
+    t_e2e = statistics.mean(e2e_ms) / 1e3 if e2e_ms else None
 
     peak, peak_src = hbm_peak()
     hbm_bytes = 2 * ranks * nbytes  # read every rank buffer once, write every rank buffer once
@@ -391,9 +353,11 @@ def main_single(args):
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": hbm_bytes},
         "cpu_baseline": cpu,
-        "e2e": {"value": round(busbw(ranks, nbytes, t_e2e), 4), "unit": "GB/s",
-                "h2d_bytes_per_step": ranks * nbytes, "d2h_bytes_per_step": ranks * nbytes,
-                "ms_per_step": round(t_e2e * 1e3, 3), "chunks": args.e2e_chunks, "result_matches_device_path": e2e_ok},
+        "e2e": None if t_e2e is None else {
+            "value": round(busbw(ranks, nbytes, t_e2e), 4), "unit": "GB/s",
+            "h2d_bytes_per_step": ranks * nbytes, "d2h_bytes_per_step": ranks * nbytes,
+            "ms_per_step": round(t_e2e * 1e3, 3), "windows": args.e2e_chunks, "result_matches_device_path": e2e_ok,
+            "api": "VirtualRanks.allreduce_host (numpy buffers, page-locked, 3-stream window pipeline)"},
         "gpu_launches": launches,
         "clocks": clocks,
         "step_ms": [round(x, 4) for x in step_ms],
@@ -402,11 +366,16 @@ def main_single(args):
 
 
 def main_multi(args):
+    """N > 1: one process per GPU (torchrun, or self-launched by main()).  The
+    line's `value` is the per-GPU bus bandwidth of the config buffer (the
+    metric: bus GB/s per GPU and % of 900); the job aggregate is reported as
+    `aggregate_busbw_gbs`."""
+    import numpy as np
     import torch
     import torch.distributed as dist
 
     from paper_1708_02188_b200.multiring import Grid
-    from paper_1708_02188_b200.runtime import RankContext, Workload, generate_input
+    from paper_1708_02188_b200.runtime import PlacedBuffer, RankContext, Workload, allreduce, generate_input
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     # one rank per GPU; a box with fewer GPUs than ranks (a functional check of the
@@ -428,8 +397,10 @@ def main_multi(args):
     n = args.elems
     tdt = torch.float32 if args.dtype == "f32" else torch.bfloat16
     esz = 4 if args.dtype == "f32" else 2
+    nbytes = n * esz
     ctx = RankContext(rank, grid, device=local, mode=args.mode, blocking=False)
-    host = torch.from_numpy(generate_input(Workload(lengths=(n,), dtype="f32", seed=0), 0, rank, n)).to(tdt)
+    host_np = generate_input(Workload(lengths=(n,), dtype="f32", seed=0), 0, rank, n)
+    host = torch.from_numpy(host_np).to(tdt)
     pristine = host.to(dev)
     work = ctx.empty(n, args.dtype)
     scratch = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -439,125 +410,181 @@ def main_multi(args):
         work.copy_(pristine)
         flush_l2(scratch)
 
+    def max_over_ranks(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
+
+    def timed(c, fn, iters, before):
+        """before() (restore / L2 flush, ends with a device spin so the host runs
+        ahead), a device flag barrier, then fn() between CUDA events on the
+        launching stream; per-iteration max over ranks, in ms."""
+        ev = []
+        for _ in range(iters):
+            before()
+            c.barrier()  # device-side: the ranks leave it together
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            fn()
+            e.record(stream)
+            ev.append((s, e))
+        torch.cuda.synchronize()
+        c.check()
+        return max_over_ranks([s.elapsed_time(e) for s, e in ev])
+
+    # correctness of the exact timed configuration (outside timing)
     restore()
     ctx.collective("allreduce", work)
     ctx.synchronize()
-    for _ in range(args.warmup):
-        restore()
-        ctx.barrier()
-        ctx.collective("allreduce", work)
-    ctx.synchronize()
+    timed(ctx, lambda: ctx.collective("allreduce", work), args.warmup, restore)
     dist.barrier()
 
     sampler = ClockSampler(local)
     if rank == 0:
         sampler.start()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     l0 = ctx.launches
-    torch.cuda.synchronize()
-    dist.barrier()
-    for s, e in ev:
-        restore()
-        ctx.barrier()  # device-side flag barrier: ranks leave it together
-        s.record(stream)
-        ctx.collective("allreduce", work)
-        e.record(stream)
-    torch.cuda.synchronize()
-    ctx.check()
+    step_ms = timed(ctx, lambda: ctx.collective("allreduce", work), args.steps, restore)
     launches = ctx.launches - l0 - args.steps  # minus the barrier launches (outside the timed region)
     clocks = sampler.stop() if rank == 0 else None
-    step_ms = torch.tensor([s.elapsed_time(e) for s, e in ev], device=dev)
-    dist.all_reduce(step_ms, op=dist.ReduceOp.MAX)
-    t = step_ms.mean().item() / 1e3
-    nbytes = n * esz
+    t = statistics.mean(step_ms) / 1e3
     bw = busbw(world, nbytes, t)
 
-    # e2e: pinned host buffer -> H2D -> allreduce -> D2H inside the timed region,
-    # pipelined over element windows (rbx_allreduce_window) on three streams
-    pinned = host.pin_memory()
-    out = torch.empty_like(host).pin_memory()
+    # the other grids of the same box size on the same buffer: config 1 (2x4) at N=8, (4,) at N=4
+    other = {}
+    for odims in {8: [(2, 4), (8,)], 4: [(4,)]}.get(world, []):
+        if odims == dims:
+            continue
+        octx = RankContext(rank, Grid(odims), device=local, mode=args.mode, blocking=False)
+        owork = octx.empty(n, args.dtype)
 
-    def h2d(lo, hi):
-        work[lo:hi].copy_(pinned[lo:hi], non_blocking=True)
+        def orestore(w=owork):
+            w.copy_(pristine)
+            flush_l2(scratch)
 
-    def d2h(lo, hi):
-        out[lo:hi].copy_(work[lo:hi], non_blocking=True)
+        timed(octx, lambda c=octx, w=owork: c.collective("allreduce", w), 3, orestore)
+        ms = timed(octx, lambda c=octx, w=owork: c.collective("allreduce", w), max(5, min(args.steps, 10)), orestore)
+        ot = statistics.mean(ms) / 1e3
+        other["x".join(map(str, odims))] = {"us": round(ot * 1e6, 2), "busbw_gbs": round(busbw(world, nbytes, ot), 2)}
+        octx.close()
 
-    def red(lo, hi, st):
-        with torch.cuda.stream(st):
-            ctx.allreduce_window(work, lo, hi)
+    # NVLink ceiling on this box, measured in the same run: every rank pushes the allreduce's
+    # bus bytes (2(N-1)/N * S per GPU, 2S/N to each peer) into every peer's copy of a registered
+    # buffer with the copy engines (cudaMemcpyAsync, one stream per peer), all ranks at once --
+    # the fastest engine in profiles/r02_nvlink_ceiling_*.jsonl, no fold, no ordering
+    ceiling = None
+    if not shared:
+        try:
+            from cuda.bindings import runtime as cr
 
-    e2e = pipelined_e2e(n, args.e2e_chunks, h2d, red, d2h, stream, args.warmup + max(3, min(args.steps, 10)),
-                        args.warmup, lambda: (flush_l2(scratch), ctx.barrier()))
-    e2e_t = torch.tensor(e2e, device=dev)
-    dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    t_e2e = e2e_t.mean().item() / 1e3
-    ctx.check()
-    # the host result of the last e2e step must equal the device path's allreduce (all ranks)
-    restore()
-    ctx.collective("allreduce", work)
-    ctx.synchronize()
-    ok = torch.tensor([1 if torch.equal(out, work.cpu()) else 0], device=dev)
-    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-    e2e_ok = bool(ok.item())
+            per_peer = (2 * nbytes // world) // 256 * 256
+            cbuf = ctx.empty(per_peer * world // 4 + 64, "f32")
+            peers = [q for q in range(world) if q != rank]
+            streams = [torch.cuda.Stream(dev) for _ in peers]
+            my = cbuf.data_ptr()
 
-    # the metric's "vs msg size" curve: the same timing (L2 flushed, device barrier,
-    # one collective between events, max over ranks) on views of one large buffer
+            def push():
+                start = torch.cuda.Event()
+                start.record(stream)
+                for q, st in zip(peers, streams):
+                    st.wait_event(start)
+                    dst = ctx.peer_pointer(cbuf, q) + rank * per_peer
+                    cr.cudaMemcpyAsync(dst, my + q * per_peer, per_peer, cr.cudaMemcpyKind.cudaMemcpyDefault,
+                                       st.cuda_stream)
+                for st in streams:
+                    stream.wait_stream(st)
+
+            timed(ctx, push, 3, lambda: flush_l2(scratch))
+            cms = timed(ctx, push, 10, lambda: flush_l2(scratch))
+            ct = statistics.median(cms) / 1e3
+            ceiling = {"gbs_per_direction": round(2 * (world - 1) / world * nbytes / ct / 1e9, 1),
+                       "us": round(ct * 1e6, 2), "bytes_per_direction": int(per_peer * (world - 1)),
+                       "engine": "copy engines: cudaMemcpyAsync push of 2S/N to every peer, one stream per peer, "
+                                 "all ranks at once (no fold, no ordering)"}
+            del cbuf
+        except Exception as exc:  # noqa: BLE001 -- cuda-python missing: report the recipe's figure
+            ceiling = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+
+    # e2e through the product API with a HOST buffer: runtime.allreduce(ctx, PlacedBuffer(numpy))
+    # -- page-locked once, H2D / kernel / D2H of element windows on three streams; every step
+    # copies the whole buffer in and the result out inside the timed region (device events)
+    e2e = None
+    if args.dtype == "f32":
+        arr = host_np.copy()
+        ems = []
+        for it in range(args.warmup + max(3, min(args.steps, 10))):
+            arr[...] = host_np
+            flush_l2(scratch)
+            ctx.barrier()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            allreduce(ctx, PlacedBuffer(arr, memory="host"))
+            e.record(stream)
+            torch.cuda.synchronize()
+            if it >= args.warmup:
+                ems.append(s.elapsed_time(e))
+        ems = max_over_ranks(ems)
+        t_e2e = statistics.mean(ems) / 1e3
+        restore()
+        ctx.collective("allreduce", work)
+        ctx.synchronize()
+        ok = torch.tensor([1 if np.array_equal(arr, work.cpu().numpy()) else 0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        e2e = {"value": round(busbw(world, nbytes, t_e2e), 3), "unit": "GB/s",
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": round(t_e2e * 1e3, 3),
+               "aggregate_gbs": round(busbw(world, nbytes, t_e2e) * world, 3),
+               "result_matches_device_path": bool(ok.item()),
+               "api": "runtime.allreduce(ctx, PlacedBuffer(numpy)): page-locked host buffer, 3-stream window pipeline"}
+
+    # the metric's "vs msg size" curve: the same timing on views of one large buffer, NCCL alongside
     curve = []
     if args.curve:
         big_n = max(CURVE_BYTES) // esz
         big = ctx.empty(big_n, args.dtype)
         big.fill_(1.0)
+        nbig = None if args.no_nccl else torch.ones(big_n, dtype=tdt, device=dev)
+        tiny = torch.zeros(1, device=dev)
         for nbytes_c in CURVE_BYTES:
             view = big[:nbytes_c // esz]
-            ts = []
-            for it in range(3 + 10):
-                flush_l2(scratch)
-                ctx.barrier()
-                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                s.record(stream)
-                ctx.collective("allreduce", view)
-                e.record(stream)
-                torch.cuda.synchronize()
-                if it >= 3:
-                    ts.append(s.elapsed_time(e))
-            tt = torch.tensor(ts, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            us = tt.median().item() * 1e3
-            curve.append({"bytes": nbytes_c, "us": round(us, 2), "busbw_gbs": round(busbw(world, nbytes_c, us / 1e6), 2)})
-        ctx.check()
-        del big
+            timed(ctx, lambda v=view: ctx.collective("allreduce", v), 3, lambda: flush_l2(scratch))
+            ms = timed(ctx, lambda v=view: ctx.collective("allreduce", v), 10, lambda: flush_l2(scratch))
+            us = statistics.median(ms) * 1e3
+            pt = {"bytes": nbytes_c, "us": round(us, 2), "busbw_gbs": round(busbw(world, nbytes_c, us / 1e6), 2)}
+            if nbig is not None:
+                nv = nbig[:nbytes_c // esz]
+                nt = []
+                for it in range(13):
+                    flush_l2(scratch)
+                    dist.all_reduce(tiny)
+                    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    s.record(stream)
+                    dist.all_reduce(nv)
+                    e.record(stream)
+                    torch.cuda.synchronize()
+                    if it >= 3:
+                        nt.append(s.elapsed_time(e))
+                nus = statistics.median(max_over_ranks(nt)) * 1e3
+                pt["nccl_us"] = round(nus, 2)
+                pt["nccl_busbw_gbs"] = round(busbw(world, nbytes_c, nus / 1e6), 2)
+            curve.append(pt)
+        del big, nbig
 
     # the reference's other two collectives on the same buffer (runtime.py:278-292):
     # busbw = (N-1)/N * S / t each (NCCL convention for reduce-scatter / all-gather)
     parts = {}
     for op in ("reduce_scatter", "allgather"):
-        ts = []
-        for it in range(3 + 10):
-            restore()
-            ctx.barrier()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record(stream)
-            ctx.collective(op, work)
-            e.record(stream)
-            torch.cuda.synchronize()
-            if it >= 3:
-                ts.append(s.elapsed_time(e))
-        tt = torch.tensor(ts, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        us = tt.median().item() * 1e3
+        timed(ctx, lambda o=op: ctx.collective(o, work), 3, restore)
+        ms = timed(ctx, lambda o=op: ctx.collective(o, work), 10, restore)
+        us = statistics.median(ms) * 1e3
         parts[op] = {"us": round(us, 2), "busbw_gbs": round((world - 1) / world * nbytes / (us / 1e6) / 1e9, 2)}
-    ctx.check()
 
     nccl = None
     if not args.no_nccl:
         nbuf = pristine.clone()
+        tiny = torch.zeros(1, device=dev)
         for _ in range(3):
             dist.all_reduce(nbuf)
         torch.cuda.synchronize()
         nt = []
-        tiny = torch.zeros(1, device=dev)
-        dist.barrier()
         for _ in range(10):
             nbuf.copy_(pristine)
             flush_l2(scratch)  # ends with a device spin: the host runs ahead
@@ -568,15 +595,29 @@ def main_multi(args):
             e.record(stream)
             torch.cuda.synchronize()
             nt.append(s.elapsed_time(e))
-        ntt = torch.tensor(nt, device=dev)
-        dist.all_reduce(ntt, op=dist.ReduceOp.MAX)
-        nccl = round(busbw(world, nbytes, ntt.median().item() / 1e3), 2)
+        nccl = round(busbw(world, nbytes, statistics.median(max_over_ranks(nt)) / 1e3), 2)
+
+    # the reference's CPU multi-ring allreduce on this box's host cores, same job, same run
+    # (rank 0; the other ranks wait at the barrier)
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        times, r_ = cpu_port_run(dims, n, budget_s=10.0)
+        tc = statistics.median(times)
+        cores = len(os.sched_getaffinity(0))
+        cpu = {"value": round(busbw(world, n * 4, tc), 4), "unit": "GB/s", "cores": min(world, cores), "kind": "port",
+               "sample": f"{len(times)} full allreduces of {n} fp32 x {world} ranks (grid {'x'.join(map(str, dims))}) "
+                         f"with the C port of the reference runtime, one thread per rank; median {tc * 1e3:.1f} ms; "
+                         f"host has {cores} cores"}
+    dist.barrier()
 
     traffic = ncu_traffic("nvlink_tx_2_25.6M_f32") if (world == 2 and n == N_ELEM and args.dtype == "f32") else None
     if rank == 0:
+        peak = ceiling.get("gbs_per_direction") if ceiling else None
+        peak_src = "measured in this run: " + ceiling["engine"] if peak else "B200_PROFILING.md measured peer copy"
+        peak = peak or MEASURED_PEER_GBS
         line = {
             "metric": "multi-ring allreduce bus GB/s vs msg size at 2/4/8 B200; % of 900 GB/s NVLink",
-            "value": round(bw * world, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "value": round(bw, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t * 1e3, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (reference generate_input, seed 0)",
             "config": {"workload": workload_name(n, args.dtype, world, dims),
@@ -584,28 +625,47 @@ def main_multi(args):
                                      "not a measurement)") if shared else f"{world} GPUs, one rank each",
                        "ranks": world, "dims": list(dims), "bytes_per_rank": nbytes, "mode": args.mode,
                        "l2": "flushed between steps (256 MiB write per rank)",
-                       "value_definition": "N * busbw, busbw = 2(N-1)/N*S/t (NCCL convention), max over ranks"},
-            "busbw_gbs": round(bw, 3), "pct_of_900": round(100 * bw / NOMINAL_NVLINK_GBS, 2),
-            "algbw_gbs": round(nbytes / t / 1e9, 3),
-            "roofline": {"bound": "nvlink", "achieved": round(bw, 2), "peak": MEASURED_PEER_GBS, "unit": "GB/s",
-                         "frac": round(bw / MEASURED_PEER_GBS, 4), "traffic": traffic,
+                       "value_definition": "per-GPU busbw = 2(N-1)/N*S/t (NCCL convention), t = max over ranks"},
+            "busbw_gbs": round(bw, 3), "aggregate_busbw_gbs": round(bw * world, 3),
+            "pct_of_900": round(100 * bw / NOMINAL_NVLINK_GBS, 2), "algbw_gbs": round(nbytes / t / 1e9, 3),
+            "other_grids": other or None,
+            "roofline": {"bound": "nvlink", "achieved": round(bw, 2), "peak": peak, "unit": "GB/s",
+                         "frac": round(bw / peak, 4), "traffic": traffic,
                          "traffic_kind": "NVLink TX bytes per launch per GPU (ncu nvltx__bytes.sum, user + protocol; "
                                          "2-GPU harness, profiles/ncu_traffic.json)" if traffic else None,
-                         "peak_source": "measured peer copy per direction (B200_PROFILING.md); nominal 900",
+                         "peak_source": peak_src, "ceiling": ceiling,
+                         "frac_of_770": round(bw / MEASURED_PEER_GBS, 4), "frac_of_900": round(bw / NOMINAL_NVLINK_GBS, 4),
                          "algorithmic_bytes_per_launch": int(2 * (world - 1) / world * nbytes)},
             "nccl_busbw_gbs": nccl,
             "curve": curve or None,
             "reduce_scatter": parts["reduce_scatter"], "allgather": parts["allgather"],
-            "cpu_baseline": None,
-            "e2e": {"value": round(busbw(world, nbytes, t_e2e) * world, 3), "unit": "GB/s",
-                    "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": round(t_e2e * 1e3, 3),
-                    "chunks": args.e2e_chunks, "result_matches_device_path": e2e_ok},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,
+            "step_ms": [round(x, 4) for x in step_ms],
         }
         print(json.dumps(line), flush=True)
     ctx.close()
     dist.destroy_process_group()
+
+
+def self_launch_command(argv, gpus: int, port: int) -> list:
+    """`python bench.py --gpus N` without torchrun: one rank per GPU through
+    torch.distributed.run, the same argv (the reference's launch() likewise
+    spawns its own N workers, runtime.py:435-589)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def self_launch(args) -> int:
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = {**os.environ, "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS", "1")}
+    return subprocess.call(self_launch_command(sys.argv[1:], args.gpus, port), env=env)
 
 
 def main():
@@ -615,6 +675,8 @@ def main():
         return
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:
         main_multi(args)
+    elif args.gpus > 1:
+        sys.exit(self_launch(args))
     else:
         main_single(args)
 

@@ -114,6 +114,11 @@ int rbx_comm_trace(rbx_comm_t *comm, uint64_t *out, int cap);
 int rbx_register_buffer(rbx_comm_t *comm, void *ptr, size_t bytes, const rbx_ipc_handle_t *handles,
                         const uint64_t *offsets, int *buf_id);
 
+/* This process's mapping of `rank`'s copy of the registered buffer that contains `buf` (same byte
+ * offset): the symmetric-memory view, for callers that move data between ranks themselves (e.g. the
+ * bench's copy-engine ceiling measurement). */
+int rbx_peer_pointer(rbx_comm_t *comm, const void *buf, int rank, void **out);
+
 /* MODE_PUSH scratch: bytes of symmetric inbox the given buffers need (host-only), and the collective
  * registration of this rank's inbox (handles/offsets of every rank, like rbx_register_buffer). */
 int64_t rbx_inbox_bytes(const int *dims, int ndims, const size_t *counts, int nbufs, int dtype);

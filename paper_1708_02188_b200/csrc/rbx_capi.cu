@@ -137,6 +137,12 @@ struct rbx_comm {
   uint64_t timeout_ns = 30ull * 1000000000ull;  // runtime.py:39 DEFAULT_TIMEOUT_S
   std::vector<RegBuf> bufs;
   std::map<std::string, CachedPlan> plans;
+  // Plans replaced while a CUDA graph may still reference them (a capture has used this
+  // communicator): kept alive until rbx_comm_destroy instead of freed.
+  std::vector<CachedPlan> retired;
+  bool captured = false;  // some launch of this communicator was recorded into a CUDA graph
+  std::vector<char*> retired_inboxes;  // virtual comms' own inboxes replaced after a capture
+  bool warned_misalign = false;
   uint64_t launches = 0;
   bool connected = false;
   int sm_count = 148;
@@ -499,13 +505,45 @@ int upload(rbx_comm* c, std::vector<rbx::Plan>& host, const std::vector<std::vec
   return RBX_OK;
 }
 
+void free_plan(CachedPlan& cp) {
+  cudaFree(cp.dev);
+  cudaFree(cp.ptrs);
+}
+
+// Drop cached plans (all, or only those using the inbox).  Plans a captured CUDA graph
+// may replay are retired (freed at destroy); otherwise they are freed after the
+// device is idle.
+int drop_plans(rbx_comm* c, bool inbox_only) {
+  if (!c->captured) RBX_CUDA(cudaDeviceSynchronize());
+  for (auto it = c->plans.begin(); it != c->plans.end();) {
+    if (inbox_only && !it->second.uses_inbox) {
+      ++it;
+      continue;
+    }
+    if (c->captured)
+      c->retired.push_back(it->second);
+    else
+      free_plan(it->second);
+    it = c->plans.erase(it);
+  }
+  return RBX_OK;
+}
+
+// Bound the plan cache (one entry per distinct buffer pointer / window / count: DDP
+// bucket rebuilds or fresh tensors would otherwise grow device memory without limit).
+constexpr size_t kMaxPlans = 512;
+int bound_plans(rbx_comm* c) { return c->plans.size() >= kMaxPlans ? drop_plans(c, false) : RBX_OK; }
+
 // Serialise launches of one communicator across streams (outside stream
 // capture; inside a graph the capture order is the user's contract).
 int order_before(rbx_comm* c, cudaStream_t stream, bool* capturing) {
   cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
   RBX_CUDA(cudaStreamIsCapturing(stream, &st));
   *capturing = st != cudaStreamCaptureStatusNone;
-  if (*capturing) return RBX_OK;
+  if (*capturing) {
+    c->captured = true;
+    return RBX_OK;
+  }
   if (!c->order_ev) RBX_CUDA(cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming));
   if (c->has_last && stream != c->last_stream) RBX_CUDA(cudaStreamWaitEvent(stream, c->order_ev, 0));
   return RBX_OK;
@@ -782,6 +820,7 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
   const std::string key = plan_key(op, mode, dtype, kp, kc) + "@" + std::to_string(lo) + ":" + std::to_string(hi);
   auto it = c->plans.find(key);
   if (it == c->plans.end()) {
+    if (int rc = bound_plans(c)) return rc;
     std::vector<rbx::Plan> host(1);
     std::vector<void*> ptrs;
     rbx::PlanSpec spec;
@@ -809,6 +848,13 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
         std::vector<char*> mine;
         for (int q = 0; q < c->nranks; ++q) mine.push_back(c->bufs[id].at[q] + off);
         spec.mis = misalign(std::vector<void*>(mine.begin(), mine.end()), es);
+        if (spec.mis < 0 && !c->warned_misalign) {
+          // correct, but every element goes through the scalar path (one CTA per segment)
+          std::fprintf(stderr, "librbx: rank %d: buffer copies are differently aligned across ranks (16-byte phase); "
+                               "this collective runs element by element -- allocate symmetric buffers at equal offsets\n",
+                       c->rank);
+          c->warned_misalign = true;
+        }
         if (push || ws) {
           const int64_t need = rbx::inbox_buffer_bytes(c->geo, (int64_t)counts[k], es);
           if (inbox_off + need > (int64_t)c->inbox_bytes)
@@ -1033,15 +1079,14 @@ int rbx_comm_destroy(rbx_comm_t* c) {
   if (!c) return RBX_OK;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
-  for (auto& kv : c->plans) {
-    cudaFree(kv.second.dev);
-    cudaFree(kv.second.ptrs);
-  }
+  for (auto& kv : c->plans) free_plan(kv.second);
+  for (auto& cp : c->retired) free_plan(cp);
   close_handles(c);
   if (c->sig_local) cudaFree(c->sig_local);
   if (c->trace_dev) cudaFree(c->trace_dev);
   if (c->order_ev) cudaEventDestroy(c->order_ev);
   if (c->inbox_owned && c->inbox_local) cudaFree(c->inbox_local);
+  for (char* p : c->retired_inboxes) cudaFree(p);
   if (c->err_host) cudaFreeHost(c->err_host);
   delete c;
   return RBX_OK;
@@ -1106,16 +1151,9 @@ int rbx_set_inbox(rbx_comm_t* c, void* ptr, size_t bytes, const rbx_ipc_handle_t
     if (rc) return rc;
     at[q] = static_cast<char*>(p) + offsets[q];
   }
-  // cached MODE_PUSH plans point into the old inbox
-  for (auto it = c->plans.begin(); it != c->plans.end();) {
-    if (it->second.uses_inbox) {
-      cudaFree(it->second.dev);
-      cudaFree(it->second.ptrs);
-      it = c->plans.erase(it);
-    } else {
-      ++it;
-    }
-  }
+  // cached MODE_PUSH / fp32-workspace plans point into the old inbox (retired, not freed,
+  // if a captured graph may still replay them; the caller keeps the old inbox alive)
+  if (int rc = drop_plans(c, true)) return rc;
   c->inbox_local = static_cast<char*>(ptr);
   c->inbox_bytes = bytes;
   c->inbox_at = at;
@@ -1142,6 +1180,16 @@ int rbx_register_buffer(rbx_comm_t* c, void* ptr, size_t bytes, const rbx_ipc_ha
   }
   c->bufs.push_back(b);
   *buf_id = (int)c->bufs.size() - 1;
+  return RBX_OK;
+}
+
+int rbx_peer_pointer(rbx_comm_t* c, const void* buf, int rank, void** out) {
+  if (!c || c->nvirtual) return fail(RBX_ERR_INVALID, "not a per-rank communicator");
+  if (rank < 0 || rank >= c->nranks) return fail(RBX_ERR_INVALID, "rank out of range");
+  int id;
+  size_t off;
+  if (int rc = find_buffer(c, buf, 1, &id, &off)) return rc;
+  *out = c->bufs[id].at[rank] + off;
   return RBX_OK;
 }
 
@@ -1269,18 +1317,14 @@ int rbx_vcollective_window(rbx_comm_t* c, void* const* bufs, size_t count, size_
     if ((int64_t)c->inbox_bytes < need) {
       RBX_CUDA(cudaSetDevice(c->device));
       RBX_CUDA(cudaDeviceSynchronize());
-      if (c->inbox_local) cudaFree(c->inbox_local);
+      if (c->captured) {  // a captured graph may replay plans that address the old inbox
+        if (c->inbox_local) c->retired_inboxes.push_back(c->inbox_local);
+      } else if (c->inbox_local) {
+        cudaFree(c->inbox_local);
+      }
       c->inbox_local = nullptr;
       c->inbox_bytes = 0;
-      for (auto pit = c->plans.begin(); pit != c->plans.end();) {
-        if (pit->second.uses_inbox) {
-          cudaFree(pit->second.dev);
-          cudaFree(pit->second.ptrs);
-          pit = c->plans.erase(pit);
-        } else {
-          ++pit;
-        }
-      }
+      if (int rc = drop_plans(c, true)) return rc;
       RBX_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->inbox_local), (size_t)need * V));
       c->inbox_owned = true;
       c->inbox_bytes = (size_t)need;
@@ -1290,6 +1334,7 @@ int rbx_vcollective_window(rbx_comm_t* c, void* const* bufs, size_t count, size_
     }
   }
   if (it == c->plans.end()) {
+    if (int rc = bound_plans(c)) return rc;
     std::string err;
     std::vector<void*> ptrs(bufs, bufs + V);
     std::vector<rbx::Plan> host(local ? 1 : V);
@@ -1345,10 +1390,12 @@ int rbx_vcollective_window(rbx_comm_t* c, void* const* bufs, size_t count, size_
   }
   if (it->second.local_fn) {  // specialised local-reduce kernel (no step table, no flags)
     void* params[] = {it->second.local_args.get()};
+    bool capturing = false;
+    if (int rc = order_before(c, (cudaStream_t)stream, &capturing)) return rc;
     RBX_CUDA(cudaLaunchKernel(it->second.local_fn, dim3((unsigned)it->second.local_grid), dim3((unsigned)c->threads),
                               params, 0, (cudaStream_t)stream));
     c->launches++;
-    return RBX_OK;
+    return order_after(c, (cudaStream_t)stream, capturing);
   }
   if (!local && (int64_t)nb * V > c->max_coresident)
     return fail(RBX_ERR_INVALID, "virtual ranks x blocks exceed co-resident CTAs");

@@ -1,0 +1,124 @@
+"""Host-buffer collectives: PlacedBuffer(memory="host") on the GPU path.
+
+Reference: the DDL object carries a `memory` placement (pkg/src/ringbox/
+runtime.py:51-69) and `allreduce(ctx, obj)` reduces it in
+place (runtime.py:295-297).  The reference only has host memory; here a host
+(numpy) buffer is reduced by the GPU kernel, so its bytes must cross PCIe both
+ways.  Done naively (copy in, reduce, copy out) the three phases serialise.
+This module pipelines them over element windows, each window a full-geometry
+allreduce of [lo, hi) (bit-identical to those elements of a whole-buffer call,
+rbx_allreduce_window), on three streams:
+
+    copy-in (H2D)  w0  w1  w2  ...
+    reduce             w0  w1  w2 ...
+    copy-out (D2H)         w0  w1  w2
+
+so PCIe runs in both directions while the NVLink kernel works on the window
+before.  The numpy memory itself is page-locked once (cudaHostRegister,
+released when the array is garbage collected) so the copies run at the host
+link's DMA rate with no staging memcpy on the CPU.
+"""
+
+from __future__ import annotations
+
+import weakref
+
+import numpy as np
+
+_REGISTERED: dict = {}  # base address -> nbytes of page-locked numpy memory
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def pin_array(arr: np.ndarray) -> None:
+    """Page-lock the memory of `arr` (cached; unregistered when the owning
+    array is collected).  Best effort: if registration fails the copies still
+    work, through the driver's pageable path."""
+    if arr.nbytes == 0:
+        return
+    base = arr
+    while isinstance(base.base, np.ndarray):
+        base = base.base
+    addr = base.__array_interface__["data"][0]
+    nbytes = base.nbytes
+    hit = _REGISTERED.get(addr)
+    if hit is not None and hit >= nbytes:
+        return
+    torch = _torch()
+    cudart = torch.cuda.cudart()
+    if hit is not None:
+        cudart.cudaHostUnregister(addr)
+        del _REGISTERED[addr]
+    rc = cudart.cudaHostRegister(addr, nbytes, 0)
+    if int(rc) != 0:
+        return
+    _REGISTERED[addr] = nbytes
+
+    def _release(a=addr):
+        if _REGISTERED.pop(a, None) is not None:
+            try:
+                _torch().cuda.cudart().cudaHostUnregister(a)
+            except Exception:  # noqa: BLE001 -- interpreter shutdown
+                pass
+
+    weakref.finalize(base, _release)
+
+
+class HostPipeline:
+    """Three streams (copy-in, reduce, copy-out) of one device."""
+
+    def __init__(self, device):
+        torch = _torch()
+        self.device = device
+        with torch.cuda.device(device):
+            self.s_in, self.s_red, self.s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+
+    def run(self, pairs, n: int, windows: int, reduce) -> None:
+        """pairs: [(host numpy array, device tensor)], every array n elements.
+        reduce(lo, hi, stream): enqueue the collective of window [lo, hi).
+        Enqueued after the caller's current stream; the current stream waits
+        for the last copy-out, then the host waits for it (the result is in
+        the numpy arrays when this returns)."""
+        torch = _torch()
+        cur = torch.cuda.current_stream(self.device)
+        hosts = []
+        for arr, _ in pairs:
+            pin_array(arr)
+            hosts.append(torch.from_numpy(arr))
+        windows = max(1, min(windows, n)) if n else 1
+        bounds = [(n * k // windows, n * (k + 1) // windows) for k in range(windows)]
+        start = torch.cuda.Event()
+        start.record(cur)
+        for s in (self.s_in, self.s_red, self.s_out):
+            s.wait_event(start)
+        for lo, hi in bounds:
+            if hi <= lo:
+                continue
+            with torch.cuda.stream(self.s_in):
+                for h, (_, d) in zip(hosts, pairs):
+                    d[lo:hi].copy_(h[lo:hi], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self.s_in)
+            self.s_red.wait_event(ev)
+            reduce(lo, hi, self.s_red)
+            ev = torch.cuda.Event()
+            ev.record(self.s_red)
+            self.s_out.wait_event(ev)
+            with torch.cuda.stream(self.s_out):
+                for h, (_, d) in zip(hosts, pairs):
+                    h[lo:hi].copy_(d[lo:hi], non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(self.s_out)
+        cur.wait_event(done)
+        cur.synchronize()
+
+
+def default_windows(nbytes: int, cap: int = 32) -> int:
+    """Pipeline depth: ~1 window per MiB up to `cap` (32 windows of a 102.4 MB
+    buffer measured best against the host-link ceiling, profiles/r01_pcie_probe_*);
+    small buffers stay one window (one launch, the LL kernel when it qualifies)."""
+    return max(1, min(cap, nbytes >> 20))

@@ -187,9 +187,12 @@ class RankContext:
         _native.check(self._L.rbx_comm_connect(self._comm, arr))
         self._registered: dict = {}  # data_ptr -> (nbytes, tensor kept alive)
         self._inbox = None
+        self._old_inboxes: list = []
         self._inbox_bytes = 0
         self._agreed: set = set()
         self._staging: dict = {}
+        self._pipe = None  # hoststage.HostPipeline, created on the first host-buffer allreduce
+        self.host_windows = int(os.environ.get("RBX_HOST_WINDOWS", "0"))  # 0: hoststage.default_windows
         self._traffic: dict = {}
         self.bytes_sent = 0
         self.plan_hash = 0
@@ -268,6 +271,12 @@ class RankContext:
         _native.check(self._L.rbx_register_buffer(self._comm, ctypes.c_void_p(ptr), nbytes, hs, offs, ctypes.byref(bid)))
         self._registered[ptr] = (nbytes, tensor)
 
+    def peer_pointer(self, tensor, rank: int) -> int:
+        """Address (in this process) of `rank`'s copy of a registered tensor."""
+        out = ctypes.c_void_p()
+        _native.check(self._L.rbx_peer_pointer(self._comm, ctypes.c_void_p(tensor.data_ptr()), rank, ctypes.byref(out)))
+        return out.value
+
     def _ensure_inbox(self, counts, dtype: str, op: str, mode: int) -> None:
         """MODE_PUSH needs a symmetric inbox (~1x the buffer bytes); grow it
         collectively when a larger buffer shows up (all ranks make the same
@@ -293,6 +302,9 @@ class RankContext:
         hs = (_native.IpcHandle * len(items))(*[_native.IpcHandle.from_raw(x[0]) for x in items])
         offs = (ctypes.c_uint64 * len(items))(*[x[1] for x in items])
         _native.check(self._L.rbx_set_inbox(self._comm, ctypes.c_void_p(inbox.data_ptr()), nbytes, hs, offs))
+        if self._inbox is not None:
+            # a CUDA graph captured earlier may still replay plans that address it
+            self._old_inboxes.append(self._inbox)
         self._inbox = inbox
         self._inbox_bytes = nbytes
 
@@ -363,6 +375,11 @@ class RankContext:
     def allreduce_window(self, tensor, lo: int, hi: int, mode: str | None = None) -> None:
         """Allreduce only elements [lo, hi) of `tensor`, with the full buffer's
         chunk geometry and order (bit-identical to those elements of a full call)."""
+        self._window(tensor, lo, hi, mode, None)
+        if self.blocking:
+            self.synchronize()
+
+    def _window(self, tensor, lo: int, hi: int, mode, stream) -> None:
         dt = _dtype_name(tensor)
         n = tensor.numel()
         m = _native.MODES[mode or self.mode]
@@ -371,10 +388,9 @@ class RankContext:
         self._ensure(tensor)
         self._agree_shape((tensor.data_ptr(), "window", n, lo, hi, dt, m))
         self._ensure_inbox([n], dt, "window", m)
+        s = self.stream() if stream is None else ctypes.c_void_p(stream.cuda_stream)
         _native.check(self._L.rbx_allreduce_window(self._comm, ctypes.c_void_p(tensor.data_ptr()), n, lo, hi,
-                                                   _native.DTYPE_CODES[dt], m, self.stream()))
-        if self.blocking:
-            self.synchronize()
+                                                   _native.DTYPE_CODES[dt], m, s))
 
     def allreduce_buckets(self, tensors, mode: str | None = None) -> None:
         """All buckets of a list in ONE launch (concurrent rings); each bucket is
@@ -427,26 +443,48 @@ class RankContext:
             self._comm = None
 
 
-def _host_roundtrip(ctx: RankContext, obj: PlacedBuffer, op: str):
-    """memory="host": H2D into a registered staging buffer, collective on the
-    GPU, D2H back into the numpy array in place."""
+_NP_DTYPES = {np.dtype(np.float32): "f32", np.dtype(np.float64): "f64", np.dtype(np.int64): "i64",
+              np.dtype(np.int32): "i32", np.dtype(np.float16): "f16"}
+
+
+def _host_collective(ctx: RankContext, obj: PlacedBuffer, op: str):
+    """memory="host" (a numpy array, reduced in place).  allreduce: the array is
+    page-locked once and streamed through a registered device buffer in element
+    windows -- H2D of window k+1, the kernel on window k and D2H of window k-1
+    run concurrently (hoststage.HostPipeline); each window is a full-geometry
+    allreduce of its elements, so the result is bit-identical to one call.
+    reduce_scatter / allgather: one H2D, the collective, one D2H."""
+    from .hoststage import HostPipeline, default_windows, pin_array
+
     torch = _torch()
     arr = obj.data
-    dt = {np.dtype(np.float32): "f32", np.dtype(np.float64): "f64", np.dtype(np.int64): "i64",
-          np.dtype(np.int32): "i32", np.dtype(np.float16): "f16"}[arr.dtype]
-    dev = ctx.staging(len(arr), dt)
-    dev.copy_(torch.from_numpy(arr), non_blocking=False)
+    if arr.dtype not in _NP_DTYPES:
+        raise ValueError(f"unsupported host dtype {arr.dtype}")
+    dt = _NP_DTYPES[arr.dtype]
+    n = len(arr)
+    dev = ctx.staging(n, dt)
+    if op == "allreduce" and n:
+        if ctx._pipe is None:
+            ctx._pipe = HostPipeline(ctx.device)
+        windows = ctx.host_windows or default_windows(arr.nbytes)
+        ctx._pipe.run([(arr, dev)], n, windows, lambda lo, hi, s: ctx._window(dev, lo, hi, None, s))
+        ctx.bytes_sent += ctx._rank_traffic(n, arr.itemsize, "allreduce")
+        ctx.check()
+        return (0, n)
+    pin_array(arr)
+    host = torch.from_numpy(arr)
+    dev.copy_(host, non_blocking=True)
     owned = ctx.collective(op, dev)
+    host.copy_(dev, non_blocking=True)
     torch.cuda.current_stream(ctx.device).synchronize()
     ctx.check()
-    arr[...] = dev.cpu().numpy()
     return owned
 
 
 def reduce_scatter(ctx: RankContext, obj: PlacedBuffer):
     """Reduce-scatter half; returns a view of this rank's owned chunk."""
     if isinstance(obj.data, np.ndarray):
-        off, length = _host_roundtrip(ctx, obj, "reduce_scatter")
+        off, length = _host_collective(ctx, obj, "reduce_scatter")
     else:
         off, length = ctx.collective("reduce_scatter", obj.data)
     return obj.data[off:off + length]
@@ -454,7 +492,7 @@ def reduce_scatter(ctx: RankContext, obj: PlacedBuffer):
 
 def allgather(ctx: RankContext, obj: PlacedBuffer) -> PlacedBuffer:
     if isinstance(obj.data, np.ndarray):
-        _host_roundtrip(ctx, obj, "allgather")
+        _host_collective(ctx, obj, "allgather")
     else:
         ctx.collective("allgather", obj.data)
     return obj
@@ -463,7 +501,7 @@ def allgather(ctx: RankContext, obj: PlacedBuffer) -> PlacedBuffer:
 def allreduce(ctx: RankContext, obj: PlacedBuffer) -> PlacedBuffer:
     """In-place sum over all ranks in the reference's reduction order (one launch)."""
     if isinstance(obj.data, np.ndarray):
-        _host_roundtrip(ctx, obj, "allreduce")
+        _host_collective(ctx, obj, "allreduce")
     else:
         ctx.collective("allreduce", obj.data)
     return obj

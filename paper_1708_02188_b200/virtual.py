@@ -75,6 +75,36 @@ class VirtualRanks:
                                                      _native.OPS[op], _native.MODES[mode],
                                                      ctypes.c_void_p(s.cuda_stream)))
 
+    def allreduce_host(self, arrays: list, mode: str = "local", windows: int | None = None) -> list:
+        """Every rank's buffer is a host (numpy) array, reduced in place: the
+        arrays are page-locked once and streamed through device buffers in
+        element windows, H2D / kernel / D2H overlapped on three streams
+        (hoststage.HostPipeline; each window bit-identical to a full call)."""
+        import torch
+
+        from .hoststage import HostPipeline, default_windows
+
+        if len(arrays) != self.nranks:
+            raise ValueError(f"need {self.nranks} arrays, got {len(arrays)}")
+        n = len(arrays[0])
+        if any(len(a) != n or a.dtype != arrays[0].dtype for a in arrays):
+            raise ValueError("virtual-rank arrays must match in length and dtype")
+        key = (n, str(arrays[0].dtype))
+        staging = getattr(self, "_staging", {})
+        self._staging = staging
+        if key not in staging:
+            tdt = torch.from_numpy(arrays[0][:0]).dtype
+            staging.clear()
+            staging[key] = [torch.empty(n, dtype=tdt, device=self.device) for _ in range(self.nranks)]
+        devs = staging[key]
+        if getattr(self, "_pipe", None) is None:
+            self._pipe = HostPipeline(self.device)
+        w = windows or default_windows(arrays[0].nbytes * self.nranks, cap=8)
+        self._pipe.run(list(zip(arrays, devs)), n, w,
+                       lambda lo, hi, s: self.collective(devs, mode=mode, stream=s, window=(lo, hi)))
+        self.check()
+        return arrays
+
     def check(self) -> None:
         _native.check(self._L.rbx_check(self._comm))
 

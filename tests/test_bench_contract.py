@@ -57,3 +57,22 @@ def test_default_arguments(monkeypatch):
     assert a.warmup >= 3  # timing rules: W >= 3
     monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4"])
     assert bench.parse_args().e2e_chunks == 32
+
+
+def test_gpus_n_without_torchrun_self_launches(monkeypatch):
+    """`python bench.py --gpus N` (no WORLD_SIZE) spawns N ranks through
+    torch.distributed.run with the same arguments -- it never silently runs the
+    1-GPU path for N > 1."""
+    cmd = bench.self_launch_command(["--gpus", "4", "--steps", "3"], 4, 29555)
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd and "--master-port=29555" in cmd
+    assert cmd[-4:] == [os.path.join(ROOT, "bench.py"), "--gpus", "4", "--steps", "3"][-4:]
+    calls = []
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "2", "--steps", "3"])
+    monkeypatch.setattr(bench.subprocess, "call", lambda c, env=None: calls.append(c) or 0)
+    monkeypatch.setattr(bench, "main_single", lambda a: (_ for _ in ()).throw(AssertionError("N=1 path ran")))
+    with pytest.raises(SystemExit) as ex:
+        bench.main()
+    assert ex.value.code == 0
+    assert len(calls) == 1 and "--nproc-per-node=2" in calls[0] and calls[0][-4:] == ["--gpus", "2", "--steps", "3"]
