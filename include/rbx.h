@@ -110,6 +110,9 @@ int rbx_comm_inject_fault(rbx_comm_t *comm, double fraction);
  * last (32..63) CTA: 0 start, 1 plan staged, 2 entry signalled, 3+3s/4+3s/5+3s step s waited/worked/
  * signalled, 30 steps done, 31 exit.  Tracing / profiling subsystem. */
 int rbx_comm_trace(rbx_comm_t *comm, uint64_t *out, int cap);
+/* Diagnostic: a 1-thread kernel on `stream` that writes the device's %globaltimer (ns, the clock of
+ * rbx_comm_trace) to the device word *dst -- brackets a collective on the device clock. */
+int rbx_stamp(uint64_t *dst, void *stream);
 /* Collective registration: every rank passes its own (ptr, bytes) and all ranks' handles/offsets. */
 int rbx_register_buffer(rbx_comm_t *comm, void *ptr, size_t bytes, const rbx_ipc_handle_t *handles,
                         const uint64_t *offsets, int *buf_id);

@@ -57,6 +57,9 @@ const void* fused_kernel_i32(int nsrc, int nlev, int maxseg);
 
 namespace {
 
+// %globaltimer into *dst (diagnostic: brackets a collective on the device clock)
+__global__ void stamp_kernel(uint64_t* dst) { *dst = rbx::global_ns(); }
+
 thread_local std::string g_err;
 thread_local int g_err_rank = -1, g_err_stage = -1;
 
@@ -192,6 +195,8 @@ struct rbx_comm {
   // env RBX_FUSED_KERNEL=0 forces the generic step interpreter
   bool fused_specialised = true;
   int pdl = 1;  // programmatic dependent launch for the fused kernel; env RBX_PDL
+  int fused_dbg = 0;  // env RBX_FUSED_DBG: experiment knobs of the fused kernel (rbx_fused.cuh FusedArgsT::dbg)
+  bool plain_launch = false;  // env RBX_PLAIN_LAUNCH=1: fused kernel through cudaLaunchKernel (no launch attributes)
 };
 
 namespace {
@@ -394,6 +399,35 @@ int coresident_blocks(int device, int threads, int* out) {
   return RBX_OK;
 }
 
+// Every kernel of the library asks for the same L1 / shared-memory split, so
+// consecutive launches of ours (barrier -> collective, bucket -> bucket) never
+// make the SMs drain and reconfigure the carveout between them.  env
+// RBX_CARVEOUT: percent of the unified L1 given to shared memory (-1: leave
+// each kernel's default).
+int set_carveouts(int device, int pct) {
+  static std::mutex mu;
+  static std::map<int, int> done;  // device -> carveout applied
+  std::lock_guard<std::mutex> lock(mu);
+  if (pct < 0) return RBX_OK;
+  auto hit = done.find(device);
+  if (hit != done.end() && hit->second == pct) return RBX_OK;
+  std::vector<const void*> fns;
+  for (int dt = RBX_F32; dt <= RBX_I32; ++dt) {
+    fns.push_back(kernel_for(dt));
+    fns.push_back(ll_kernel_for(dt, 1));
+    fns.push_back(ll_kernel_for(dt, RBX_MAX_RANKS));
+    for (int n : {2, 4, 8})
+      for (int l = 1; l <= 3; ++l)
+        for (int ms : {1, RBX_FUSED_MAXSEG}) fns.push_back(fused_kernel_for(dt, n, l, ms));
+    for (int v : {2, 4, 8})
+      for (int l = 1; l <= 3; ++l) fns.push_back(local_kernel_for(dt, v, l));
+  }
+  for (const void* f : fns)
+    if (f) RBX_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+  done[device] = pct;
+  return RBX_OK;
+}
+
 int common_init(rbx_comm* c, const int* dims, int ndims, int device, int threads) {
   std::string err;
   if (!c->geo.init(dims, ndims, &err)) return fail(RBX_ERR_INVALID, err);
@@ -410,6 +444,8 @@ int common_init(rbx_comm* c, const int* dims, int ndims, int device, int threads
   if (const char* t = std::getenv("RBX_LOCAL_GENERIC")) c->local_specialised = std::atoi(t) == 0;
   if (const char* t = std::getenv("RBX_FUSED_KERNEL")) c->fused_specialised = std::atoi(t) != 0;
   if (const char* t = std::getenv("RBX_PDL")) c->pdl = std::atoi(t) != 0;
+  if (const char* t = std::getenv("RBX_FUSED_DBG")) c->fused_dbg = std::atoi(t);
+  if (const char* t = std::getenv("RBX_PLAIN_LAUNCH")) c->plain_launch = std::atoi(t) != 0;
   if (const char* t = std::getenv("RBX_LOCAL_CTAS_PER_SM")) c->local_ctas_per_sm = std::atoi(t);
   if (const char* t = std::getenv("RBX_BYTES_PER_CTA")) c->bytes_per_cta = (size_t)std::max(1L, std::atol(t));
   if (const char* t = std::getenv("RBX_MIN_BLOCKS")) c->min_blocks = std::max(1, std::atoi(t));
@@ -419,6 +455,9 @@ int common_init(rbx_comm* c, const int* dims, int ndims, int device, int threads
   if (const char* t = std::getenv("RBX_LL_ONESHOT_BYTES")) c->ll_oneshot_bytes = std::atol(t);
   RBX_CUDA(cudaSetDevice(device));
   RBX_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+  int carveout = 50;  // 114 KB of shared memory: covers the step kernel's staged plan at 2 CTAs per SM
+  if (const char* t = std::getenv("RBX_CARVEOUT")) carveout = std::atoi(t);
+  if (int rc2 = set_carveouts(device, carveout)) return rc2;
   int rc = coresident_blocks(device, threads, &c->max_coresident);
   if (rc) return rc;
   if (const char* t = std::getenv("RBX_TRACE")) {
@@ -592,11 +631,13 @@ int fused_launch(rbx_comm* c, CachedPlan& cp, cudaStream_t stream, int nb) {
     cp.fused1->timeout_ns = c->timeout_ns;
     cp.fused1->trace = c->trace_dev;
     cp.fused1->fault_milli = c->fault_milli;
+    cp.fused1->dbg = c->fused_dbg;
     argp = cp.fused1.get();
   } else {
     cp.fusedN->timeout_ns = c->timeout_ns;
     cp.fusedN->trace = c->trace_dev;
     cp.fusedN->fault_milli = c->fault_milli;
+    cp.fusedN->dbg = c->fused_dbg;
     argp = cp.fusedN.get();
   }
   c->fault_milli = -1;
@@ -614,7 +655,10 @@ int fused_launch(rbx_comm* c, CachedPlan& cp, cudaStream_t stream, int nb) {
   void* params[] = {argp};
   bool capturing = false;
   if (int rc = order_before(c, stream, &capturing)) return rc;
-  RBX_CUDA(cudaLaunchKernelExC(&cfg, cp.fused_fn, params));
+  if (c->plain_launch)
+    RBX_CUDA(cudaLaunchKernel(cp.fused_fn, cfg.gridDim, cfg.blockDim, params, 0, stream));
+  else
+    RBX_CUDA(cudaLaunchKernelExC(&cfg, cp.fused_fn, params));
   c->launches++;
   return order_after(c, stream, capturing);
 }
@@ -879,7 +923,11 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
     cp.uses_inbox = push || ws;
     int rc = upload(c, host, {ptrs}, &cp, dtype);
     if (rc) return rc;
-    const bool fused = (mode == RBX_MODE_FUSED || mode == RBX_MODE_AUTO) && op == RBX_OP_ALLREDUCE && !push && !ws;
+    // RING_DIMS over a one-dimensional grid is the same single ring fold as FUSED (same
+    // order, same pushes): both go through the specialised kernel
+    const bool one_ring = mode == RBX_MODE_RING_DIMS && c->geo.active_dims().size() == 1;
+    const bool fused = (mode == RBX_MODE_FUSED || mode == RBX_MODE_AUTO || one_ring) && op == RBX_OP_ALLREDUCE &&
+                       !push && !ws;
     if (fused && c->fused_specialised) {
       const int nseg = host[0].nsteps ? host[0].steps[0].nseg : 0;
       const int maxseg = nseg <= 1 ? 1 : RBX_FUSED_MAXSEG;
@@ -1180,6 +1228,12 @@ int rbx_register_buffer(rbx_comm_t* c, void* ptr, size_t bytes, const rbx_ipc_ha
   }
   c->bufs.push_back(b);
   *buf_id = (int)c->bufs.size() - 1;
+  return RBX_OK;
+}
+
+int rbx_stamp(uint64_t* dst, void* stream) {
+  stamp_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(dst);
+  RBX_CUDA(cudaGetLastError());
   return RBX_OK;
 }
 

@@ -56,6 +56,8 @@ struct FusedArgsT {
   ErrRecord* err;
   unsigned long long* trace;
   int fault_milli;                    // rbx_comm_inject_fault: -1 off
+  int dbg;                            // experiment knobs (env RBX_FUSED_DBG; 0 in production): bit0 relaxed
+                                      // exit signal, bit1 no exit wait, bit2 fence.sys before exit, bit3 no entry
   FusedSeg seg[MAXSEG];
 };
 
@@ -180,8 +182,8 @@ __global__ void __launch_bounds__(512, 1) rbx_fused_kernel(const __grid_constant
   const uint64_t t0 = global_ns();
   if (tr) tr[1] = t0;
   // ENTRY (slot 0): relaxed -- nothing of this launch has been written yet
-  if ((int)threadIdx.x < a.npeers) st_relaxed_sys(a.peer_sig[threadIdx.x] + flag_index(0, a.me, b), e);
-  if ((int)threadIdx.x < a.npeers) {
+  if ((int)threadIdx.x < a.npeers && !(a.dbg & 8)) st_relaxed_sys(a.peer_sig[threadIdx.x] + flag_index(0, a.me, b), e);
+  if ((int)threadIdx.x < a.npeers && !(a.dbg & 8)) {
     const int q = a.peer_rank[threadIdx.x];
     if (!fused_spin(my_sig + flag_index(0, q, b), e, abort_word, t0, a.timeout_ns)) {
       s_fail = 1;
@@ -238,9 +240,14 @@ __global__ void __launch_bounds__(512, 1) rbx_fused_kernel(const __grid_constant
   // EXIT (slot 1): release my pushes to every peer's matched CTA, then wait for theirs.
   // st.release.sys is cumulative over the CTA's writes ordered before it by bar.sync.
   __syncthreads();
-  if ((int)threadIdx.x < a.npeers) st_release_sys(a.peer_sig[threadIdx.x] + flag_index(1, a.me, b), e);
-  if (tr) tr[5] = global_ns();
   if ((int)threadIdx.x < a.npeers) {
+    if (a.dbg & 1)
+      st_relaxed_sys(a.peer_sig[threadIdx.x] + flag_index(1, a.me, b), e);
+    else
+      st_release_sys(a.peer_sig[threadIdx.x] + flag_index(1, a.me, b), e);
+  }
+  if (tr) tr[5] = global_ns();
+  if ((int)threadIdx.x < a.npeers && !(a.dbg & 2)) {
     const int q = a.peer_rank[threadIdx.x];
     if (!fused_spin(my_sig + flag_index(1, q, b), e, abort_word, t0, a.timeout_ns)) {
       s_fail = 1;
@@ -265,6 +272,7 @@ __global__ void __launch_bounds__(512, 1) rbx_fused_kernel(const __grid_constant
       *(volatile uint32_t*)(my_sig + SigLayout::epoch_off) = e;
     }
   }
+  if (a.dbg & 4) __threadfence_system();
   if (tr) tr[31] = global_ns();
 }
 
