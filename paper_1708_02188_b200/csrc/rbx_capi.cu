@@ -25,6 +25,7 @@
 #include "rbx_plan.h"
 
 #include "rbx_fused.cuh"
+#include "rbx_rings.cuh"
 #include "rbx_local.cuh"
 #include "rbx_ll.cuh"
 
@@ -53,6 +54,12 @@ const void* fused_kernel_i64(int nsrc, int nlev, int maxseg);
 const void* fused_kernel_bf16(int nsrc, int nlev, int maxseg);
 const void* fused_kernel_f16(int nsrc, int nlev, int maxseg);
 const void* fused_kernel_i32(int nsrc, int nlev, int maxseg);
+const void* rings_kernel_f32();
+const void* rings_kernel_f64();
+const void* rings_kernel_i64();
+const void* rings_kernel_bf16();
+const void* rings_kernel_f16();
+const void* rings_kernel_i32();
 }  // namespace rbx
 
 namespace {
@@ -108,6 +115,9 @@ struct CachedPlan {
   const void* fused_fn = nullptr;
   std::shared_ptr<rbx::FusedArgsT<1>> fused1;
   std::shared_ptr<rbx::FusedArgsT<RBX_FUSED_MAXSEG>> fusedN;
+  // specialised RING_DIMS kernel (rbx_rings.cuh): one stage per grid dimension, matched waits
+  const void* rings_fn = nullptr;
+  std::shared_ptr<rbx::RingsArgs> rings;
 };
 
 struct LLKey {  // cached MODE_LL launch arguments: buffers, count, dtype
@@ -197,6 +207,7 @@ struct rbx_comm {
   int pdl = 1;  // programmatic dependent launch for the fused kernel; env RBX_PDL
   int fused_dbg = 0;  // env RBX_FUSED_DBG: experiment knobs of the fused kernel (rbx_fused.cuh FusedArgsT::dbg)
   bool plain_launch = false;  // env RBX_PLAIN_LAUNCH=1: fused kernel through cudaLaunchKernel (no launch attributes)
+  bool rings_specialised = true;  // RING_DIMS through rbx_rings_kernel where possible; env RBX_RINGS_KERNEL=0: generic
 };
 
 namespace {
@@ -341,6 +352,59 @@ bool fused_args_from_plan(const rbx_comm* c, const rbx::Plan& p, const std::vect
   return true;
 }
 
+const void* rings_kernel_for(int dtype) {
+  switch (dtype) {
+    case RBX_F32: return rbx::rings_kernel_f32();
+    case RBX_F64: return rbx::rings_kernel_f64();
+    case RBX_I64: return rbx::rings_kernel_i64();
+    case RBX_BF16: return rbx::rings_kernel_bf16();
+    case RBX_F16: return rbx::rings_kernel_f16();
+    case RBX_I32: return rbx::rings_kernel_i32();
+    default: return nullptr;
+  }
+}
+
+// Arguments of the RING_DIMS kernel from a RING_DIMS allreduce plan (rbx_plan.cpp):
+// steps 0..m-1 are the reduce-scatter stages, m..2m-2 the all-gathers, the last step
+// is the exit wait.  Every wait becomes a MATCHED wait (rbx_rings.cuh explains why that
+// is sufficient); slots are the step indices.  Ring sizes must be 2, 4 or 8.
+bool rings_args_from_plan(const rbx_comm* c, const rbx::Plan& p, const std::vector<void*>& table, rbx::RingsArgs* a) {
+  std::memset(a, 0, sizeof(*a));
+  const int ns = p.nsteps - 1;  // data stages
+  if (ns < 3 || ns > RBX_RINGS_MAX_STAGES || p.steps[ns].nseg != 0) return false;
+  a->me = c->rank;
+  a->nstages = ns;
+  a->my_sig = c->sig[c->rank];
+  for (int q = 0; q < c->nranks; ++q) a->sig[q] = c->sig[q];
+  a->nentry = p.nentry;
+  for (int i = 0; i < p.nentry; ++i) a->entry_peer[i] = p.entry_peers[i];
+  for (int s = 0; s <= ns; ++s) {
+    const rbx::Step& st = p.steps[s];
+    for (int w = 0; w < st.nwait; ++w)
+      if (p.waits[st.wait0 + w].slot != s) return false;
+    if (s == ns) {
+      a->nexit = st.nwait;
+      for (int w = 0; w < st.nwait; ++w) a->exit_peer[w] = p.waits[st.wait0 + w].peer;
+      break;
+    }
+    if (st.nseg != 1) return false;
+    const rbx::Seg& sg = p.segs[st.seg0];
+    if (sg.acc || sg.nlev != 1 || !(sg.nsrc == 1 || sg.nsrc == 2 || sg.nsrc == 4 || sg.nsrc == 8)) return false;
+    rbx::RingStage& R = a->st[s];
+    R.off = sg.off;
+    R.len = sg.len;
+    R.nsrc = sg.nsrc;
+    R.ndst = sg.ndst;
+    for (int j = 0; j < sg.nsrc; ++j) R.src[j] = static_cast<const char*>(table[sg.tbl + sg.src[j]]);
+    for (int d = 0; d < sg.ndst; ++d) R.dst[d] = static_cast<char*>(table[sg.tbl + sg.dst[d]]);
+    R.nwait = s == 0 ? 0 : (uint8_t)st.nwait;  // stage 0 waits on the entry flags
+    for (int w = 0; s > 0 && w < st.nwait; ++w) R.wait_peer[w] = p.waits[st.wait0 + w].peer;
+    R.nsig = (uint8_t)st.nsig;
+    for (int k = 0; k < st.nsig; ++k) R.sig_peer[k] = p.sigs[st.sig0 + k];
+  }
+  return true;
+}
+
 const void* local_kernel_for(int dtype, int v, int nlev) {
   switch (dtype) {
     case RBX_F32: return rbx::local_kernel_f32(v, nlev);
@@ -421,6 +485,7 @@ int set_carveouts(int device, int pct) {
         for (int ms : {1, RBX_FUSED_MAXSEG}) fns.push_back(fused_kernel_for(dt, n, l, ms));
     for (int v : {2, 4, 8})
       for (int l = 1; l <= 3; ++l) fns.push_back(local_kernel_for(dt, v, l));
+    fns.push_back(rings_kernel_for(dt));
   }
   for (const void* f : fns)
     if (f) RBX_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
@@ -446,6 +511,7 @@ int common_init(rbx_comm* c, const int* dims, int ndims, int device, int threads
   if (const char* t = std::getenv("RBX_PDL")) c->pdl = std::atoi(t) != 0;
   if (const char* t = std::getenv("RBX_FUSED_DBG")) c->fused_dbg = std::atoi(t);
   if (const char* t = std::getenv("RBX_PLAIN_LAUNCH")) c->plain_launch = std::atoi(t) != 0;
+  if (const char* t = std::getenv("RBX_RINGS_KERNEL")) c->rings_specialised = std::atoi(t) != 0;
   if (const char* t = std::getenv("RBX_LOCAL_CTAS_PER_SM")) c->local_ctas_per_sm = std::atoi(t);
   if (const char* t = std::getenv("RBX_BYTES_PER_CTA")) c->bytes_per_cta = (size_t)std::max(1L, std::atol(t));
   if (const char* t = std::getenv("RBX_MIN_BLOCKS")) c->min_blocks = std::max(1, std::atoi(t));
@@ -659,6 +725,29 @@ int fused_launch(rbx_comm* c, CachedPlan& cp, cudaStream_t stream, int nb) {
     RBX_CUDA(cudaLaunchKernel(cp.fused_fn, cfg.gridDim, cfg.blockDim, params, 0, stream));
   else
     RBX_CUDA(cudaLaunchKernelExC(&cfg, cp.fused_fn, params));
+  c->launches++;
+  return order_after(c, stream, capturing);
+}
+
+int rings_launch(rbx_comm* c, CachedPlan& cp, cudaStream_t stream, int nb) {
+  cp.rings->timeout_ns = c->timeout_ns;
+  cp.rings->trace = c->trace_dev;
+  cp.rings->fault_milli = c->fault_milli;
+  c->fault_milli = -1;
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)nb);
+  cfg.blockDim = dim3((unsigned)c->threads);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = c->pdl;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* params[] = {cp.rings.get()};
+  bool capturing = false;
+  if (int rc = order_before(c, stream, &capturing)) return rc;
+  RBX_CUDA(cudaLaunchKernelExC(&cfg, cp.rings_fn, params));
   c->launches++;
   return order_after(c, stream, capturing);
 }
@@ -948,6 +1037,21 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
         if (ok) cp.fused_fn = fn;
       }
     }
+    // the paper's per-dimension rings through the specialised kernel: whole aligned buffer,
+    // 4/8-byte types (16-bit types keep fp32 stage partials in workspaces: generic kernel)
+    if (mode == RBX_MODE_RING_DIMS && op == RBX_OP_ALLREDUCE && !one_ring && !ws && nbufs == 1 && whole &&
+        spec.mis == 0 && c->rings_specialised) {
+      const void* fn = rings_kernel_for(dtype);
+      int per_sm = 0;
+      if (fn) RBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, c->threads, 0));
+      if (fn && per_sm * c->sm_count >= c->nblocks) {
+        cp.rings = std::make_shared<rbx::RingsArgs>();
+        if (rings_args_from_plan(c, host[0], ptrs, cp.rings.get()))
+          cp.rings_fn = fn;
+        else
+          cp.rings.reset();
+      }
+    }
     it = c->plans.emplace(key, cp).first;
   }
   // CTAs per call: enough to cover the bytes (bandwidth), few for small
@@ -962,6 +1066,7 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
   }
   if (nb > c->nblocks) nb = c->nblocks;
   if (it->second.fused_fn) return fused_launch(c, it->second, stream, nb);
+  if (it->second.rings_fn) return rings_launch(c, it->second, stream, nb);
   return launch(c, it->second, dtype, stream, false, nb);
 }
 

@@ -1,6 +1,7 @@
 // Instantiations of the specialised FUSED kernel (rbx_fused.cuh) for dtype f16:
-// one TU per dtype so the builds run in parallel.
+// one TU per dtype so the builds run in parallel.  Also the RING_DIMS kernel (rbx_rings.cuh).
 #include "rbx_fused.cuh"
+#include "rbx_rings.cuh"
 
 namespace rbx {
 const void* fused_kernel_f16(int nsrc, int nlev, int maxseg) {
@@ -12,4 +13,6 @@ const void* fused_kernel_f16(int nsrc, int nlev, int maxseg) {
 #undef RBX_FUSED_CASE
   return nullptr;
 }
+// 16-bit RING_DIMS keeps fp32 stage partials in workspaces: generic step kernel
+const void* rings_kernel_f16() { return nullptr; }
 }  // namespace rbx

@@ -1,6 +1,7 @@
 // Instantiations of the specialised FUSED kernel (rbx_fused.cuh) for dtype i64:
-// one TU per dtype so the builds run in parallel.
+// one TU per dtype so the builds run in parallel.  Also the RING_DIMS kernel (rbx_rings.cuh).
 #include "rbx_fused.cuh"
+#include "rbx_rings.cuh"
 
 namespace rbx {
 const void* fused_kernel_i64(int nsrc, int nlev, int maxseg) {
@@ -12,4 +13,5 @@ const void* fused_kernel_i64(int nsrc, int nlev, int maxseg) {
 #undef RBX_FUSED_CASE
   return nullptr;
 }
+const void* rings_kernel_i64() { return reinterpret_cast<const void*>(&rbx_rings_kernel<unsigned long long>); }
 }  // namespace rbx
