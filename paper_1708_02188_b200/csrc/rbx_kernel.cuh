@@ -269,20 +269,23 @@ __device__ __noinline__ void fold_body(const SegCtx& sc, int64_t body_off, int64
   }
   for (int64_t v = v0 + threadIdx.x; v < v1; v += stride) {
     FoldState<T, VEC, NLEV> st[U];
+    // every operand is defined on every path (zero for vectors past the end): an
+    // operand array that is only conditionally written is what made ptxas spill it
+    const bool full = v + (int64_t)(U - 1) * blockDim.x < v1;
 #pragma unroll
     for (int j0 = 0; j0 < NSRC; j0 += B) {
       int4 raw[U][B];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t idx = v + (int64_t)u * blockDim.x;
-        if (idx < v1) {
 #pragma unroll
-          for (int k = 0; k < B; ++k)
-            if (j0 + k < NSRC) {
-              const char* p = NSRC > 8 ? ((const char* volatile*)sc.src)[j0 + k] : sc.src[j0 + k];
-              raw[u][k] = ld_stream(p + base + idx * 16);
-            }
-        }
+        for (int k = 0; k < B; ++k)
+          if (j0 + k < NSRC) {
+            const char* p = NSRC > 8 ? ((const char* volatile*)sc.src)[j0 + k] : sc.src[j0 + k];
+            raw[u][k] = (full || idx < v1) ? ld_stream(p + base + idx * 16) : make_int4(0, 0, 0, 0);
+          } else {
+            raw[u][k] = make_int4(0, 0, 0, 0);
+          }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u)
