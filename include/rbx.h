@@ -113,6 +113,11 @@ int rbx_comm_trace(rbx_comm_t *comm, uint64_t *out, int cap);
 /* Diagnostic: a 1-thread kernel on `stream` that writes the device's %globaltimer (ns, the clock of
  * rbx_comm_trace) to the device word *dst -- brackets a collective on the device clock. */
 int rbx_stamp(uint64_t *dst, void *stream);
+/* Profiling harness: `rank`'s share of a FUSED allreduce of bufs[0..N) (any GPUs with peer access from
+ * the current device) through the specialised kernel with the flag protocol off, on the current device.
+ * Single process, no peer ever waits: ncu can replay it (it must never wrap a multi-rank run). */
+int rbx_fused_harness(const int *dims, int ndims, int rank, void *const *bufs, size_t count, int dtype, int nblocks,
+                      int threads, void *stream);
 /* Collective registration: every rank passes its own (ptr, bytes) and all ranks' handles/offsets. */
 int rbx_register_buffer(rbx_comm_t *comm, void *ptr, size_t bytes, const rbx_ipc_handle_t *handles,
                         const uint64_t *offsets, int *buf_id);

@@ -177,7 +177,8 @@ struct rbx_comm {
   // 1 x 512 threads per SM measured 0.967-0.972 of the copy peak vs 0.925-0.928 at the
   // occupancy limit (2 per SM) on config 2 (profiles/r01_local_ctas_per_sm.txt).
   int local_ctas_per_sm = 1;
-  bool local_specialised = true;  // MODE_LOCAL uses rbx_local_kernel where the shape has one; env RBX_LOCAL_GENERIC=1
+  bool local_specialised = true;
+  int local_hint = 0;  // cache policy of the local kernel's streams (rbx_local.cuh LocalArgs::hint); env RBX_LOCAL_HINT  // MODE_LOCAL uses rbx_local_kernel where the shape has one; env RBX_LOCAL_GENERIC=1
   // MODE_PUSH inboxes: this rank's (registered, symmetric) and every rank's mapping
   char* inbox_local = nullptr;
   size_t inbox_bytes = 0;
@@ -507,6 +508,7 @@ int common_init(rbx_comm* c, const int* dims, int ndims, int device, int threads
   if (const char* t = std::getenv("RBX_TAIL_SPLIT")) c->tail_split = std::max(1, std::atoi(t));
   if (const char* t = std::getenv("RBX_FENCE_EVERY")) c->fence_every = std::max(0, std::atoi(t));
   if (const char* t = std::getenv("RBX_LOCAL_GENERIC")) c->local_specialised = std::atoi(t) == 0;
+  if (const char* t = std::getenv("RBX_LOCAL_HINT")) c->local_hint = std::atoi(t);
   if (const char* t = std::getenv("RBX_FUSED_KERNEL")) c->fused_specialised = std::atoi(t) != 0;
   if (const char* t = std::getenv("RBX_PDL")) c->pdl = std::atoi(t) != 0;
   if (const char* t = std::getenv("RBX_FUSED_DBG")) c->fused_dbg = std::atoi(t);
@@ -1336,6 +1338,62 @@ int rbx_register_buffer(rbx_comm_t* c, void* ptr, size_t bytes, const rbx_ipc_ha
   return RBX_OK;
 }
 
+int rbx_fused_harness(const int* dims, int ndims, int rank, void* const* bufs, size_t count, int dtype, int nblocks,
+                      int threads, void* stream) {
+  // profiling harness: rank `rank`'s share of a FUSED allreduce through the specialised
+  // kernel, with the flag protocol switched off (no entry/exit waits), so a profiler can
+  // replay it without a peer; bufs[q] may live on any GPU with peer access
+  rbx_comm tmp;
+  std::string err;
+  if (!tmp.geo.init(dims, ndims, &err)) return fail(RBX_ERR_INVALID, err);
+  const int es = dtype_size(dtype);
+  if (!es) return fail(RBX_ERR_INVALID, "unknown dtype");
+  if (rank < 0 || rank >= tmp.geo.nranks) return fail(RBX_ERR_INVALID, "rank out of range");
+  int dev = 0;
+  RBX_CUDA(cudaGetDevice(&dev));
+  static std::mutex mu;
+  static std::map<int, uint32_t*> scratch;  // per device: a signal area nobody else uses
+  static std::map<int, rbx::ErrRecord*> errs;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!scratch.count(dev)) {
+      uint32_t* p = nullptr;
+      RBX_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), rbx::SigLayout::bytes));
+      RBX_CUDA(cudaMemset(p, 0, rbx::SigLayout::bytes));
+      scratch[dev] = p;
+      rbx::ErrRecord* e = nullptr;
+      RBX_CUDA(cudaMalloc(reinterpret_cast<void**>(&e), sizeof(rbx::ErrRecord)));
+      RBX_CUDA(cudaMemset(e, 0, sizeof(rbx::ErrRecord)));
+      errs[dev] = e;
+    }
+  }
+  tmp.rank = rank;
+  tmp.nranks = tmp.geo.nranks;
+  tmp.threads = threads > 0 ? threads : 512;
+  tmp.sig.assign(tmp.nranks, scratch[dev]);
+  std::vector<void*> table(bufs, bufs + tmp.nranks);
+  std::unique_ptr<rbx::Plan> plan(new rbx::Plan);
+  rbx::PlanSpec spec;
+  spec.op = rbx::OP_ALLREDUCE;
+  spec.mode = rbx::MODE_FUSED;
+  spec.vec = 16 / es;
+  spec.mis = misalign(table, es);
+  if (!rbx::build_plan(tmp.geo, rank, (int64_t)count, spec, 0, plan.get(), true, &err)) return fail(RBX_ERR_INVALID, err);
+  const void* fn = fused_kernel_for(dtype, tmp.nranks, (int)tmp.geo.active_dims().size(), 1);
+  if (!fn) return fail(RBX_ERR_UNSUPPORTED, "no specialised fused kernel for this grid");
+  rbx::FusedArgsT<1> a;
+  if (!fused_args_from_plan(&tmp, *plan, table, tmp.threads, &a)) return fail(RBX_ERR_UNSUPPORTED, "plan shape");
+  a.timeout_ns = 1000000000ull;
+  a.err = errs[dev];
+  a.trace = nullptr;
+  a.fault_milli = -1;
+  a.dbg = 1 | 2 | 8;  // relaxed exit flag into the scratch area, no exit wait, no entry handshake
+  void* params[] = {&a};
+  RBX_CUDA(cudaLaunchKernel(fn, dim3((unsigned)(nblocks > 0 ? nblocks : 148)), dim3((unsigned)tmp.threads), params, 0,
+                            (cudaStream_t)stream));
+  return RBX_OK;
+}
+
 int rbx_stamp(uint64_t* dst, void* stream) {
   stamp_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(dst);
   RBX_CUDA(cudaGetLastError());
@@ -1537,6 +1595,7 @@ int rbx_vcollective_window(rbx_comm_t* c, void* const* bufs, size_t count, size_
       const void* fn = local_kernel_for(dtype, V, (int)c->geo.active_dims().size());
       auto args = std::make_shared<rbx::LocalArgs>();
       if (fn && local_args_from_plan(host[0], ptrs, args.get())) {
+        args->hint = c->local_hint;
         int per_sm = 0;
         RBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, c->threads, 0));
         cp.local_fn = fn;

@@ -21,6 +21,8 @@ struct LocalSeg {
 
 struct LocalArgs {
   int nseg;
+  int hint;  // cache policy of the streaming loads/stores (env RBX_LOCAL_HINT): 0 .cg/.cg, 1 .cs/.cs,
+             // 2 L2::evict_first policy on both, 3 .nc L1::no_allocate loads + .cs stores
   int64_t total_vec;
   char* dst[RBX_MAX_RANKS];  // every rank's buffer
   LocalSeg seg[RBX_LOCAL_MAX_SEGS];
@@ -30,9 +32,34 @@ struct LocalArgs {
   uint8_t scalar_seg[2 * RBX_LOCAL_MAX_SEGS * 8];
 };
 
+__device__ __forceinline__ int4 ld_hint(const char* p, int hint, uint64_t pol) {
+  int4 v;
+  if (hint == 1)
+    asm volatile("ld.global.cs.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  else if (hint == 2)
+    asm volatile("ld.global.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(pol));
+  else
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_hint(char* p, int4 v, int hint, uint64_t pol) {
+  if (hint == 2)
+    asm volatile("st.global.L2::cache_hint.v4.s32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w), "l"(pol)
+                 : "memory");
+  else
+    asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
 template <typename T, int V, int NLEV>
 __global__ void __launch_bounds__(512) rbx_local_kernel(const __grid_constant__ LocalArgs a) {
   constexpr int VEC = Traits<T>::VEC;
+  uint64_t pol = 0;
+  if (a.hint == 2) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int s = 0;
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < a.total_vec; v += stride) {
@@ -40,8 +67,13 @@ __global__ void __launch_bounds__(512) rbx_local_kernel(const __grid_constant__ 
     const LocalSeg& sg = a.seg[s];
     const int64_t byte = (sg.body_off + (v - sg.vec_begin) * VEC) * (int64_t)sizeof(T);
     int4 raw[V];
+    if (a.hint == 0) {
 #pragma unroll
-    for (int j = 0; j < V; ++j) raw[j] = ld_stream(sg.src[j] + byte);
+      for (int j = 0; j < V; ++j) raw[j] = ld_stream(sg.src[j] + byte);
+    } else {
+#pragma unroll
+      for (int j = 0; j < V; ++j) raw[j] = ld_hint(sg.src[j] + byte, a.hint, pol);
+    }
     FoldState<T, VEC, NLEV> st;
 #pragma unroll
     for (int j = 0; j < V; ++j) {
@@ -51,8 +83,13 @@ __global__ void __launch_bounds__(512) rbx_local_kernel(const __grid_constant__ 
       st.feed(sg.ctrl[j], x);
     }
     const int4 packed = pack_result(st);
+    if (a.hint == 0) {
 #pragma unroll
-    for (int d = 0; d < V; ++d) __stcg(reinterpret_cast<int4*>(a.dst[d] + byte), packed);
+      for (int d = 0; d < V; ++d) __stcg(reinterpret_cast<int4*>(a.dst[d] + byte), packed);
+    } else {
+#pragma unroll
+      for (int d = 0; d < V; ++d) st_hint(a.dst[d] + byte, packed, a.hint, pol);
+    }
   }
   if (blockIdx.x == 0) {
     for (int i = threadIdx.x; i < a.nscalar; i += blockDim.x) {
