@@ -222,7 +222,7 @@ def run_reference(args):
     t = statistics.mean(timed)
     nbytes = args.elems * 4
     bw = busbw(ranks, nbytes, t)
-    value = bw * (n_gpus if n_gpus > 1 else 1)
+    value = bw  # per-(virtual-)GPU bus bandwidth, the same definition as the GPU arm's `value`
     cores = len(os.sched_getaffinity(0))
     line = {
         "metric": "multi-ring allreduce bus GB/s vs msg size at 2/4/8 B200; % of 900 GB/s NVLink",
@@ -230,7 +230,9 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference generate_input, seed 0)",
         "config": {"workload": workload_name(args.elems, "f32", ranks, dims), "placement": f"CPU, {ranks} threads",
-                   "ranks": ranks, "dims": list(dims), "bytes_per_rank": nbytes},
+                   "ranks": ranks, "dims": list(dims), "bytes_per_rank": nbytes,
+                   "value_definition": "per-rank busbw = 2(R-1)/R*S/t (NCCL convention), t = one full allreduce"},
+        "aggregate_busbw_gbs": round(bw * ranks, 4),
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": min(ranks, cores), "kind": "port",
                          "sample": f"{args.steps} full allreduces of {args.elems} fp32 x {ranks} ranks "
                                    f"(oracle/rbx_oracle.c orc_runtime_port, {ranks} threads, host has {cores} cores)"},

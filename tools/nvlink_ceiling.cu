@@ -53,23 +53,27 @@ __device__ __forceinline__ int4 ldcg(const int4* p) {
   return v;
 }
 
-// grid-stride copy over all pairs, U 16-byte loads in flight per thread
+// grid-stride copy over all pairs, U 16-byte loads in flight per thread.  The pairs are
+// INTERLEAVED (vector i of the job belongs to pair i % np): at every moment every CTA
+// talks to every peer, as the allreduce kernels do.  (A blocked layout, pair = i / n,
+// makes all SMs of every GPU target the same peer at once: with 4 GPUs three of them
+// then converge on one destination and the measured rate halves.)
 template <int U>
 __global__ void __launch_bounds__(512) copy_pairs(const __grid_constant__ Pairs P) {
-  const long per = P.n;
-  const long total = per * P.np;
+  const long np = P.np;
+  const long total = P.n * np;
   const long stride = (long)gridDim.x * blockDim.x * U;
   for (long base = (long)blockIdx.x * blockDim.x * U + threadIdx.x; base < total; base += stride) {
     int4 v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const long i = base + (long)u * blockDim.x;
-      if (i < total) v[u] = ldcg(P.src[i / per] + i % per);
+      if (i < total) v[u] = ldcg(P.src[i % np] + i / np);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const long i = base + (long)u * blockDim.x;
-      if (i < total) __stcg(P.dst[i / per] + i % per, v[u]);
+      if (i < total) __stcg(P.dst[i % np] + i / np, v[u]);
     }
   }
 }
@@ -91,8 +95,8 @@ __global__ void bulk_pairs(const __grid_constant__ Pairs P) {
   long t = blockIdx.x;
   int s = 0;
   for (; t < total; t += gridDim.x) {
-    const int p = (int)(t / tiles_per);
-    const long off = (t % tiles_per) * TILE;
+    const int p = (int)(t % P.np);  // interleaved over the peers (see copy_pairs)
+    const long off = (t / P.np) * TILE;
     // stage s free once its previous store has read it
     asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(STAGES - 1) : "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[s])), "n"(TILE) : "memory");
