@@ -209,6 +209,7 @@ struct rbx_comm {
   int fused_dbg = 0;  // env RBX_FUSED_DBG: experiment knobs of the fused kernel (rbx_fused.cuh FusedArgsT::dbg)
   bool plain_launch = false;  // env RBX_PLAIN_LAUNCH=1: fused kernel through cudaLaunchKernel (no launch attributes)
   bool rings_specialised = true;  // RING_DIMS through rbx_rings_kernel where possible; env RBX_RINGS_KERNEL=0: generic
+  bool rings_gpu_fence = true;    // local-only stages signal after a GPU-scope fence; env RBX_RINGS_GPU_FENCE=0: sys release
 };
 
 namespace {
@@ -401,6 +402,7 @@ bool rings_args_from_plan(const rbx_comm* c, const rbx::Plan& p, const std::vect
     R.nwait = s == 0 ? 0 : (uint8_t)st.nwait;  // stage 0 waits on the entry flags
     for (int w = 0; s > 0 && w < st.nwait; ++w) R.wait_peer[w] = p.waits[st.wait0 + w].peer;
     R.nsig = (uint8_t)st.nsig;
+    R.local_only = (uint8_t)(c->rings_gpu_fence && sg.ndst == 1 && sg.dst[0] == c->rank);
     for (int k = 0; k < st.nsig; ++k) R.sig_peer[k] = p.sigs[st.sig0 + k];
   }
   return true;
@@ -514,6 +516,7 @@ int common_init(rbx_comm* c, const int* dims, int ndims, int device, int threads
   if (const char* t = std::getenv("RBX_FUSED_DBG")) c->fused_dbg = std::atoi(t);
   if (const char* t = std::getenv("RBX_PLAIN_LAUNCH")) c->plain_launch = std::atoi(t) != 0;
   if (const char* t = std::getenv("RBX_RINGS_KERNEL")) c->rings_specialised = std::atoi(t) != 0;
+  if (const char* t = std::getenv("RBX_RINGS_GPU_FENCE")) c->rings_gpu_fence = std::atoi(t) != 0;
   if (const char* t = std::getenv("RBX_LOCAL_CTAS_PER_SM")) c->local_ctas_per_sm = std::atoi(t);
   if (const char* t = std::getenv("RBX_BYTES_PER_CTA")) c->bytes_per_cta = (size_t)std::max(1L, std::atol(t));
   if (const char* t = std::getenv("RBX_MIN_BLOCKS")) c->min_blocks = std::max(1, std::atoi(t));

@@ -130,6 +130,10 @@ def main():
             line["efficiency"] = round(args.t1_ms / t_ms, 4)  # bench.py:45-56
             line["overhead_ms"] = round(t_ms - args.t1_ms, 3)
         print(json.dumps(line), flush=True)
+    if dp is not None:
+        dp.close()
+    if dp is not None and dp.ctx is not None:
+        dp.ctx.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -14,3 +14,7 @@ for v in ld16 ld4; do
   done
 done
 timeout 600 python bench.py --gpus 4 --steps 20 --warmup 5 --curve 0 --no-cpu-baseline --no-nccl > gpurun_out/h_bench4_ld8.json 2>> gpurun_out/h.err
+timeout 900 python -m pytest tests/test_gpu_multi.py -m gpu -q -x -k "all_decompositions or full_size" > gpurun_out/h_pytest_multi.log 2>&1; echo "rc=$?" >> gpurun_out/h_pytest_multi.log
+for g in 1 0; do
+  RBX_RINGS_GPU_FENCE=$g timeout 600 python bench.py --gpus 4 --steps 20 --warmup 5 --curve 0 --no-cpu-baseline --no-nccl --mode ring_dims > gpurun_out/h_bench4_rings_gpufence$g.json 2>> gpurun_out/h.err
+done
