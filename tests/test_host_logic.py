@@ -1,0 +1,45 @@
+"""Host-side logic of round 2 on CPU: the host-buffer pipeline's window count,
+the crash fraction of fault injection (the reference's crash_phase, runtime.py:
+429-432), and the bench's per-GPU value definition in the reference arm."""
+
+import numpy as np
+import pytest
+
+from paper_1708_02188_b200.hoststage import default_windows
+from paper_1708_02188_b200.multiring import Grid
+from paper_1708_02188_b200.runtime import _crash_fraction, multiring_schedule
+
+
+def test_default_windows():
+    assert default_windows(0) == 1
+    assert default_windows(4096) == 1  # small buffers: one window (one launch, LL if eligible)
+    assert default_windows(3 << 20) == 3
+    assert default_windows(102_400_000) == 32  # the bench's 102.4 MB: capped
+    assert default_windows(8 * 102_400_000, cap=8) == 8
+
+
+class _Ctx:
+    def __init__(self, dims):
+        self.grid = Grid(dims)
+
+    def schedule_for(self, n):
+        return multiring_schedule(self.grid, n)
+
+
+@pytest.mark.parametrize("dims,phases", [((4,), 6), ((2, 2), 4), ((2, 2, 2), 6), ((2, 4), 8)])
+def test_crash_fraction_follows_the_reference_phase_count(dims, phases):
+    ctx = _Ctx(dims)
+    assert len(ctx.schedule_for(100).phases) == phases  # 2 * sum(d - 1), multiring.py:170-211
+    assert _crash_fraction(ctx, 100, 1) == pytest.approx(1 / phases)
+    assert _crash_fraction(ctx, 100, 0) == 0.0
+    assert _crash_fraction(ctx, 100, None) == 0.0
+    assert _crash_fraction(ctx, 100, 10 * phases) == 1.0  # past the end: the whole collective
+    assert _crash_fraction(ctx, 0, 3) == 0.0  # empty buffer: nothing to move
+
+
+def test_host_dtype_table_covers_the_reference_dtypes():
+    from paper_1708_02188_b200.runtime import _NP_DTYPES
+
+    for dt in ("f32", "f64", "i64"):  # runtime.py:37
+        assert dt in _NP_DTYPES.values()
+    assert _NP_DTYPES[np.dtype(np.float32)] == "f32"
