@@ -5,7 +5,7 @@ the local-reduce and LL kernels, on small ragged buffers, twice (epochs and
 tile counters advanced), and every rank's bits are compared with the
 reference-order fold.  Meant to run under compute-sanitizer
 (memcheck / racecheck / synccheck / initcheck); on this sandbox's GPU pool the
-sanitizer is closed (tools/r72.sh shows the refusal), so it runs bare.
+sanitizer is closed (tools/gpurun/r72.sh shows the refusal), so it runs bare.
 
   [compute-sanitizer --tool memcheck] python tests/sanitize_workload.py [--modes local,fused,...]
 """
