@@ -1,6 +1,6 @@
 #!/bin/bash
 # round-2: what makes the fused kernel's completion slow (device-clock brackets, n=1)
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 run() { timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node=2 --master-addr=127.0.0.1 --master-port=$1 tools/gap_probe.py; }
 export GAP_SIZES=1,25600000
 for v in 0 1 2 3 4 11; do RBX_FUSED_DBG=$v run $((29700+v)) > gpurun_out/d_gap_dbg$v.jsonl 2>> gpurun_out/d_gap.err; done

@@ -1,6 +1,6 @@
 #!/bin/bash
 # round-2: configs 3 (bf16), 4 (ResNet-101 buckets) and 5 (ResNet-50 step) with the specialised kernels
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 tr() { n=$1; shift; timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$n --master-addr=127.0.0.1 --master-port=$((29800+RANDOM%100)) "$@"; }
 for n in 2 4; do
   tr $n tools/buckets.py --iters 20 > gpurun_out/g_buckets_$n.jsonl 2>> gpurun_out/g.err

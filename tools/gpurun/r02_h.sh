@@ -1,6 +1,6 @@
 #!/bin/bash
 # round-2: interpreter parity after the spill fix, local-kernel cache hints (N=1), fused-kernel ncu harness
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 timeout 900 python -m pytest tests/test_gpu_virtual.py -m gpu -q -x > gpurun_out/h_pytest_virtual.log 2>&1; echo "rc=$?" >> gpurun_out/h_pytest_virtual.log
 for h in 0 1 2 3; do
   RBX_LOCAL_HINT=$h timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/h_bench1_hint$h.json 2>> gpurun_out/h.err
