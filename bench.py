@@ -451,6 +451,27 @@ def main_multi(args):
     t = statistics.mean(step_ms) / 1e3
     bw = busbw(world, nbytes, t)
 
+    # the same collective replayed from a CUDA graph (how a training step captured whole runs it,
+    # dp.MultiringDataParallel.capture): capture once, time replays the same way
+    graph_replay = None
+    try:
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            ctx.collective("allreduce", work)
+        stream.wait_stream(side)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            ctx.collective("allreduce", work)
+        gms = timed(ctx, graph.replay, 3, restore)
+        gms = timed(ctx, graph.replay, max(5, min(args.steps, 10)), restore)
+        gt = statistics.mean(gms) / 1e3
+        graph_replay = {"us": round(gt * 1e6, 2), "busbw_gbs": round(busbw(world, nbytes, gt), 2)}
+        del graph
+    except Exception as exc:  # noqa: BLE001 -- reported, not fatal
+        graph_replay = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+
     # the other grids of the same box size on the same buffer: config 1 (2x4) at N=8, (4,) at N=4
     other = {}
     for odims in {8: [(2, 4), (8,)], 4: [(4,)]}.get(world, []):
@@ -634,6 +655,7 @@ def main_multi(args):
             "busbw_gbs": round(bw, 3), "aggregate_busbw_gbs": round(bw * world, 3),
             "pct_of_900": round(100 * bw / NOMINAL_NVLINK_GBS, 2), "algbw_gbs": round(nbytes / t / 1e9, 3),
             "other_grids": other or None,
+            "graph_replay": graph_replay,
             "roofline": {"bound": "nvlink", "achieved": round(bw, 2), "peak": peak, "unit": "GB/s",
                          "frac": round(bw / peak, 4), "traffic": traffic,
                          "traffic_kind": "NVLink TX bytes per launch per GPU (ncu nvltx__bytes.sum, user + protocol; "

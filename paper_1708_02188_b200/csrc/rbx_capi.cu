@@ -844,8 +844,18 @@ int ll_launch(rbx_comm* c, const std::vector<int>& ranks, void* const* bufs, siz
   if (int rc = order_before(c, stream, &capturing)) return rc;
   if (cooperative) {
     RBX_CUDA(cudaLaunchCooperativeKernel(fn, grid, block, params, 0, stream));
-  } else {
-    RBX_CUDA(cudaLaunchKernel(fn, grid, block, params, 0, stream));
+  } else {  // per-rank form: programmatic dependent launch, like the specialised kernels
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = c->pdl;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    RBX_CUDA(cudaLaunchKernelExC(&cfg, fn, params));
   }
   c->launches++;
   return order_after(c, stream, capturing);

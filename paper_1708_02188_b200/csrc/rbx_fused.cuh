@@ -61,8 +61,6 @@ struct FusedArgsT {
   FusedSeg seg[MAXSEG];
 };
 
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // One pass of U vectors per thread starting at step vector `lo`: all NSRC x U
 // loads first, then the folds, then NDST x U stores.  FULL: every vector is in

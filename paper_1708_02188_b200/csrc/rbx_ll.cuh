@@ -233,6 +233,7 @@ __global__ void __launch_bounds__(512, 1) rbx_ll_kernel(const __grid_constant__ 
   const int64_t cap = a.cap;
   __shared__ uint32_t s_epoch;
   __shared__ int s_fail, s_peer;
+  pdl_wait();  // before any memory access (programmatic dependent launch)
   // timeline of thread 0 of the first and last CTA of the first hosted rank:
   // [0] start [1] epoch read [3] pushed [4] folded [5] gathered [30] done [31] exit
   unsigned long long* tr = nullptr;
@@ -247,6 +248,7 @@ __global__ void __launch_bounds__(512, 1) rbx_ll_kernel(const __grid_constant__ 
     s_peer = -1;
   }
   __syncthreads();
+  pdl_launch_dependents();
   if (a.fault == 0) return;  // injected crash before any data moved
   LLWait wt{s_epoch, global_ns(), a.timeout_ns, (volatile uint32_t*)(R.my_sig + SigLayout::abort_off), false, -1};
   if (tr) tr[1] = global_ns();
