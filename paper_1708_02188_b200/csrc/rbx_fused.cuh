@@ -57,7 +57,8 @@ struct FusedArgsT {
   unsigned long long* trace;
   int fault_milli;                    // rbx_comm_inject_fault: -1 off
   int dbg;                            // experiment knobs (env RBX_FUSED_DBG; 0 in production): bit0 relaxed
-                                      // exit signal, bit1 no exit wait, bit2 fence.sys before exit, bit3 no entry
+                                      // exit signal, bit1 no exit wait, bit2 fence.sys before exit, bit3 no entry,
+                                      // bit4 static round-robin tiles instead of dynamic claiming (safe)
   FusedSeg seg[MAXSEG];
 };
 
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(512, 1) rbx_fused_kernel(const __grid_constant
   unsigned int* ctr = reinterpret_cast<unsigned int*>(my_sig + SigLayout::tiles_off);
   for (int64_t t = b; t < tlimit;) {
     unsigned int nxt = 0;
-    if (threadIdx.x == 0 && ntiles > nb) nxt = (unsigned)nb + atomicAdd(ctr, 1u);
+    if (threadIdx.x == 0 && ntiles > nb && !(a.dbg & 16)) nxt = (unsigned)nb + atomicAdd(ctr, 1u);
     const int64_t lo = t * tile;
     int s_cur = 0;  // segment of the tile's first vector
     if (MAXSEG > 1)
@@ -221,6 +222,10 @@ __global__ void __launch_bounds__(512, 1) rbx_fused_kernel(const __grid_constant
         fused_pass<T, NSRC, NLEV, U, false, MAXSEG>(a, s_cur, p);
     }
     if (ntiles <= nb) break;  // one tile per CTA, no counter
+    if (a.dbg & 16) {         // A/B: static round-robin ownership (CTA b: tiles b, b+nb, ...)
+      t += nb;
+      continue;
+    }
     __syncthreads();
     if (threadIdx.x == 0) s_next = (int)nxt;
     __syncthreads();

@@ -118,6 +118,8 @@ def main():
             "loss": float(loss.item()),
             "hook_buckets": hook_state.buckets if hook_state else None,
         }), flush=True)
+    if hook_state is not None:
+        hook_state.ctx.close()  # before the process-group teardown (close communicators first)
     if world > 1:
         dist.destroy_process_group()
 
