@@ -451,3 +451,102 @@ def test_fused_kernel_misaligned_windows_buckets(world):
             else:
                 parts = [orc.generate_input(21, 0, r, n, dtype) for r in range(world)]
                 assert dig == orc.sha256(orc.closed_form_allreduce(g, parts)), (rank, kind, dims, dtype)
+
+
+def _random_cases(world, seed=2024, count=10):
+    """Seeded random cases for the specialised kernels: lengths that do not
+    divide by the grid (ragged reference chunks), views 0-3 elements past a
+    16-byte boundary, windows, every dtype, FUSED and RING_DIMS."""
+    rng = np.random.default_rng(seed + world)
+    grids = [tuple(d) for d in orc.factorizations(world, 3)]
+    cases = []
+    for k in range(count):
+        dims = grids[int(rng.integers(len(grids)))]
+        dtype = ["f32", "f64", "i64", "bf16"][int(rng.integers(4))]
+        mode = ["fused", "ring_dims"][int(rng.integers(2))]
+        n = int(rng.integers(1, 300_000))
+        shift = int(rng.integers(0, 4)) if mode == "fused" else 0
+        window = None
+        if mode == "fused" and rng.random() < 0.4:
+            lo = int(rng.integers(0, n))
+            window = (lo, int(rng.integers(lo, n + 1)))
+        cases.append({"dims": dims, "dtype": dtype, "mode": mode, "n": n, "shift": shift, "window": window, "seed": k})
+    return cases
+
+
+def _rand_input(case, rank):
+    if case["dtype"] == "bf16":
+        x = np.random.default_rng(1000 * case["seed"] + rank).standard_normal(case["n"]).astype(np.float32)
+        return orc.bf16_round(x)
+    return orc.generate_input(case["seed"], 1, rank, case["n"], case["dtype"])
+
+
+def _rand_main(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1708_02188_b200.multiring import Grid
+    from paper_1708_02188_b200.runtime import RankContext
+
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dev = rank_device(rank)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = []
+    try:
+        for case in _random_cases(world):
+            ctx = RankContext(rank, Grid(case["dims"]), device=dev, mode=case["mode"], nblocks=32)
+            x = _rand_input(case, rank)
+            base = ctx.empty(case["n"] + 4, case["dtype"])
+            t = base[case["shift"]:case["shift"] + case["n"]]
+            src = torch.from_numpy(x.view(np.int16)).view(torch.bfloat16) if case["dtype"] == "bf16" else torch.from_numpy(x)
+            t.copy_(src)
+            if case["window"]:
+                ctx.allreduce_window(t, *case["window"])
+            else:
+                ctx.collective("allreduce", t)
+            got = t.view(torch.int16).cpu().numpy() if case["dtype"] == "bf16" else t.cpu().numpy()
+            out.append(orc.sha256(got))
+            ctx.close()
+        q.put((rank, "ok", out))
+    except Exception:  # noqa: BLE001
+        import traceback
+
+        q.put((rank, "error", traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_specialised_kernels_randomised(world):
+    """rbx_fused_kernel / rbx_rings_kernel on seeded random shapes: every grid of
+    the world, f32/f64/i64/bf16, ragged lengths, misaligned views, windows --
+    each rank's buffer equal to the reference-order fold (bf16: the fp32-
+    accumulate policy) bit for bit; outside a window the input is untouched."""
+    if cuda_count() < 1:
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_rand_main, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=900) for _ in range(world)), key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+    for item in res:
+        assert item[1] == "ok", item[2]
+    for k, case in enumerate(_random_cases(world)):
+        g = orc.Grid(case["dims"])
+        parts = [_rand_input(case, r) for r in range(world)]
+        want = [orc.bf16_allreduce(g, parts)] * world if case["dtype"] == "bf16" else \
+            [orc.closed_form_allreduce(g, parts)] * world
+        for r in range(world):
+            w = want[r].copy()
+            if case["window"]:
+                lo, hi = case["window"]
+                w = parts[r].copy()
+                w[lo:hi] = want[r][lo:hi]
+            assert res[r][2][k] == orc.sha256(w), (r, case)
