@@ -19,10 +19,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def nvml_counters(handle, pynvml):
-    """(tx_bytes, rx_bytes) summed over links, from NVML field values (KiB units)."""
+def nvml_counters(handle, pynvml, kind="DATA"):
+    """(tx_bytes, rx_bytes) summed over links, from NVML field values (KiB units).
+    kind DATA: payload only; RAW: payload + protocol (headers, read requests, acks)."""
     fids = []
-    for name in ("NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX", "NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX"):
+    for name in (f"NVML_FI_DEV_NVLINK_THROUGHPUT_{kind}_TX", f"NVML_FI_DEV_NVLINK_THROUGHPUT_{kind}_RX"):
         fids.append(getattr(pynvml, name, None))
     if None in fids:
         return None
@@ -97,6 +98,7 @@ def main():
     dist.barrier()
     time.sleep(0.5)
     c0 = nvml_counters(h, pynvml)
+    r0 = nvml_counters(h, pynvml, "RAW")
     src = "nvml"
     raw0 = ""
     if c0 is None:
@@ -115,6 +117,7 @@ def main():
     dist.barrier()
     time.sleep(0.5)
     c1 = nvml_counters(h, pynvml) if src == "nvml" else smi_counters(rank)[0]
+    r1 = nvml_counters(h, pynvml, "RAW") if src == "nvml" else None
     kt = sum(s.elapsed_time(e) for s, e in ts) / len(ts) / 1e3
     S = args.elems * 4
     alg = 2 * (world - 1) / world * S
@@ -126,6 +129,13 @@ def main():
         row.update({"nvlink_tx_bytes_per_allreduce": tx, "nvlink_rx_bytes_per_allreduce": rx,
                     "tx_over_alg": round(tx / alg, 4), "rx_over_alg": round(rx / alg, 4),
                     "achieved_tx_gbs": round(tx / kt / 1e9, 1), "achieved_rx_gbs": round(rx / kt / 1e9, 1)})
+        if r0 and r1:
+            rtx = (r1[0] - r0[0]) / args.iters
+            rrx = (r1[1] - r0[1]) / args.iters
+            row.update({"nvlink_raw_tx_bytes_per_allreduce": rtx, "nvlink_raw_rx_bytes_per_allreduce": rrx,
+                        "raw_over_data_tx": round(rtx / tx, 4) if tx else None,
+                        "raw_over_data_rx": round(rrx / rx, 4) if rx else None,
+                        "raw_tx_gbs": round(rtx / kt / 1e9, 1), "raw_rx_gbs": round(rrx / kt / 1e9, 1)})
     else:
         row["nvml"] = "NVLink throughput fields unavailable"
         row["smi_raw_head"] = raw0[:600]
