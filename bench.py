@@ -175,6 +175,37 @@ def flush_l2(scratch):
     torch.cuda._sleep(SPIN_CYCLES)
 
 
+def host_link_ms(pairs, dev, stream, iters=5, before=None):
+    """The host link's ceiling for the e2e step, measured in the same run: the same bytes
+    copied H2D and D2H at the same time on two streams (pinned memory, no kernel).
+    pairs: [(pinned host tensor, device tensor)]; returns the median ms."""
+    import torch
+
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    back = [torch.empty_like(h).pin_memory() for h, _ in pairs]
+    scratch_dev = [torch.empty_like(d) for _, d in pairs]
+    ts = []
+    for _ in range(iters):
+        if before:
+            before()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        s_in.wait_event(s)
+        s_out.wait_event(s)
+        with torch.cuda.stream(s_in):
+            for (h, _), d in zip(pairs, scratch_dev):
+                d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s_out):
+            for (_, d), b in zip(pairs, back):
+                b.copy_(d, non_blocking=True)
+        stream.wait_stream(s_in)
+        stream.wait_stream(s_out)
+        e.record(stream)
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e))
+    return statistics.median(ts)
+
+
 def workload_name(n: int, dtype: str, ranks: int, dims) -> str:
     """Same string on every arm (ours / --impl reference) for the same job."""
     return f"config2: {n} {dtype}/rank, {ranks} ranks, grid {'x'.join(map(str, dims))}"
@@ -324,6 +355,8 @@ def main_single(args):
         torch.cuda.synchronize()
         e2e_ok = all(np.array_equal(a, w.cpu().numpy()) for a, w in zip(arrays[:2], work[:2]))
     t_e2e = statistics.mean(e2e_ms) / 1e3 if e2e_ms else None
+    hl = host_link_ms([(h.pin_memory(), w) for h, w in zip(host, work)], dev, stream,
+                      before=lambda: flush_l2(scratch)) if e2e_ms else None
 
     peak, peak_src = hbm_peak()
     hbm_bytes = 2 * ranks * nbytes  # read every rank buffer once, write every rank buffer once
@@ -359,6 +392,7 @@ def main_single(args):
             "value": round(busbw(ranks, nbytes, t_e2e), 4), "unit": "GB/s",
             "h2d_bytes_per_step": ranks * nbytes, "d2h_bytes_per_step": ranks * nbytes,
             "ms_per_step": round(t_e2e * 1e3, 3), "windows": args.e2e_chunks, "result_matches_device_path": e2e_ok,
+            "host_link_ms": round(hl, 3), "frac_of_host_link": round(hl / (t_e2e * 1e3), 4),
             "api": "VirtualRanks.allreduce_host (numpy buffers, page-locked, 3-stream window pipeline)"},
         "gpu_launches": launches,
         "clocks": clocks,
@@ -552,7 +586,10 @@ def main_multi(args):
         ctx.synchronize()
         ok = torch.tensor([1 if np.array_equal(arr, work.cpu().numpy()) else 0], device=dev)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        hl = max_over_ranks([host_link_ms([(host.pin_memory(), work)], dev, stream,
+                                          before=lambda: (flush_l2(scratch), ctx.barrier()))])[0]
         e2e = {"value": round(busbw(world, nbytes, t_e2e), 3), "unit": "GB/s",
+               "host_link_ms": round(hl, 3), "frac_of_host_link": round(hl / (t_e2e * 1e3), 4),
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": round(t_e2e * 1e3, 3),
                "aggregate_gbs": round(busbw(world, nbytes, t_e2e) * world, 3),
                "result_matches_device_path": bool(ok.item()),
