@@ -76,6 +76,8 @@ def lib() -> ctypes.CDLL:
     _sig(L.rbx_comm_trace, c_int, _VP, ctypes.POINTER(ctypes.c_uint64), c_int)
     _sig(L.rbx_comm_inject_fault, c_int, _VP, ctypes.c_double)
     _sig(L.rbx_stamp, c_int, _VP, _VP)
+    _sig(L.rbx_host_register, c_int, _VP, c_size)
+    _sig(L.rbx_host_unregister, c_int, _VP)
     _sig(L.rbx_fused_harness, c_int, _INTP, c_int, c_int, ctypes.POINTER(_VP), c_size, c_int, c_int, c_int, _VP)
     _sig(L.rbx_register_buffer, c_int, _VP, _VP, c_size, HP, ctypes.POINTER(ctypes.c_uint64), _INTP)
     _sig(L.rbx_peer_pointer, c_int, _VP, _VP, c_int, ctypes.POINTER(_VP))
@@ -101,7 +103,7 @@ EXPORTED = [
     "rbx_version", "rbx_last_error", "rbx_chunk_bounds", "rbx_owned_region", "rbx_fold_order", "rbx_plan_describe",
     "rbx_device_count", "rbx_enable_peer_access", "rbx_alloc_symmetric", "rbx_free", "rbx_export_buffer", "rbx_comm_create",
     "rbx_comm_connect", "rbx_comm_destroy", "rbx_comm_set_timeout", "rbx_comm_info", "rbx_comm_trace",
-    "rbx_comm_inject_fault", "rbx_stamp", "rbx_fused_harness",
+    "rbx_comm_inject_fault", "rbx_stamp", "rbx_fused_harness", "rbx_host_register", "rbx_host_unregister",
     "rbx_register_buffer", "rbx_peer_pointer", "rbx_inbox_bytes", "rbx_set_inbox",
     "rbx_allreduce", "rbx_reduce_scatter", "rbx_allgather", "rbx_allreduce_buckets", "rbx_allreduce_window",
     "rbx_barrier", "rbx_check", "rbx_vcomm_create", "rbx_vcollective", "rbx_vcollective_window",

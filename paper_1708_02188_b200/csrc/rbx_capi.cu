@@ -1407,6 +1407,25 @@ int rbx_fused_harness(const int* dims, int ndims, int rank, void* const* bufs, s
   return RBX_OK;
 }
 
+int rbx_host_register(void* ptr, size_t bytes) {
+  const cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterDefault);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();  // not sticky: do not leave it for the next caller's error check
+    if (e == cudaErrorHostMemoryAlreadyRegistered) return RBX_OK;
+    return fail(RBX_ERR_CUDA, std::string("cudaHostRegister: ") + cudaGetErrorString(e));
+  }
+  return RBX_OK;
+}
+
+int rbx_host_unregister(void* ptr) {
+  const cudaError_t e = cudaHostUnregister(ptr);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fail(RBX_ERR_CUDA, std::string("cudaHostUnregister: ") + cudaGetErrorString(e));
+  }
+  return RBX_OK;
+}
+
 int rbx_stamp(uint64_t* dst, void* stream) {
   stamp_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(dst);
   RBX_CUDA(cudaGetLastError());

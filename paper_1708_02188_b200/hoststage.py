@@ -14,7 +14,7 @@ rbx_allreduce_window), on three streams:
     copy-out (D2H)         w0  w1  w2
 
 so PCIe runs in both directions while the NVLink kernel works on the window
-before.  The numpy memory itself is page-locked once (cudaHostRegister,
+before.  The numpy memory itself is page-locked once (rbx_host_register,
 released when the array is garbage collected) so the copies run at the host
 link's DMA rate with no staging memcpy on the CPU.
 """
@@ -48,20 +48,22 @@ def pin_array(arr: np.ndarray) -> None:
     hit = _REGISTERED.get(addr)
     if hit is not None and hit >= nbytes:
         return
-    torch = _torch()
-    cudart = torch.cuda.cudart()
+    import ctypes
+
+    from . import _native
+
+    L = _native.lib()
     if hit is not None:
-        cudart.cudaHostUnregister(addr)
+        L.rbx_host_unregister(ctypes.c_void_p(addr))
         del _REGISTERED[addr]
-    rc = cudart.cudaHostRegister(addr, nbytes, 0)
-    if int(rc) != 0:
-        return
+    if L.rbx_host_register(ctypes.c_void_p(addr), nbytes) != 0:
+        return  # the copies still work, through the driver's pageable path
     _REGISTERED[addr] = nbytes
 
     def _release(a=addr):
         if _REGISTERED.pop(a, None) is not None:
             try:
-                _torch().cuda.cudart().cudaHostUnregister(a)
+                _native.lib().rbx_host_unregister(ctypes.c_void_p(a))
             except Exception:  # noqa: BLE001 -- interpreter shutdown
                 pass
 
