@@ -119,8 +119,9 @@ class HostPipeline:
         cur.synchronize()
 
 
-def default_windows(nbytes: int, cap: int = 32) -> int:
-    """Pipeline depth: ~1 window per MiB up to `cap` (32 windows of a 102.4 MB
-    buffer measured best against the host-link ceiling, profiles/r01_pcie_probe_*);
-    small buffers stay one window (one launch, the LL kernel when it qualifies)."""
+def default_windows(nbytes: int, cap: int = 16) -> int:
+    """Pipeline depth: ~1 window per MiB up to `cap` (for a 102.4 MB buffer at N=2,
+    8 / 16 / 64 windows reach 0.948 / 0.956 / 0.890 of the host link measured in the
+    same run, profiles/r02_host_windows_2gpu.jsonl); small buffers stay one window
+    (one launch, the LL kernel when it qualifies)."""
     return max(1, min(cap, nbytes >> 20))

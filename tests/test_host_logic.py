@@ -14,7 +14,7 @@ def test_default_windows():
     assert default_windows(0) == 1
     assert default_windows(4096) == 1  # small buffers: one window (one launch, LL if eligible)
     assert default_windows(3 << 20) == 3
-    assert default_windows(102_400_000) == 32  # the bench's 102.4 MB: capped
+    assert default_windows(102_400_000) == 16  # the bench's 102.4 MB: capped
     assert default_windows(8 * 102_400_000, cap=8) == 8
 
 
