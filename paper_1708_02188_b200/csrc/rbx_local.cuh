@@ -22,7 +22,8 @@ struct LocalSeg {
 struct LocalArgs {
   int nseg;
   int hint;  // cache policy of the streaming loads/stores (env RBX_LOCAL_HINT): 0 .cg/.cg, 1 .cs/.cs,
-             // 2 L2::evict_first policy on both, 3 .nc L1::no_allocate loads + .cs stores
+             // 2 L2::evict_first policy on both, 3 .nc L1::no_allocate loads + .cs stores,
+             // 4 as 3 with an L2 256-byte prefetch hint on the loads
   int64_t total_vec;
   char* dst[RBX_MAX_RANKS];  // every rank's buffer
   LocalSeg seg[RBX_LOCAL_MAX_SEGS];
@@ -40,6 +41,10 @@ __device__ __forceinline__ int4 ld_hint(const char* p, int hint, uint64_t pol) {
     asm volatile("ld.global.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                  : "l"(p), "l"(pol));
+  else if (hint == 4)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
   else
     asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
