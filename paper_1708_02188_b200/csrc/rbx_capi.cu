@@ -192,7 +192,7 @@ struct rbx_comm {
   // measured slower than two-shot at every size (4 KB: 21 vs 13 us event time at N=2,
   // profiles/r01_ll_*), the launch/teardown floor dominates and it folds N x the elements.
   int64_t ll_oneshot_bytes = 0;
-  int ll_words_per_thread = 4;        // CTAs per LL call = words / (threads * this); env RBX_LL_WPT
+  int ll_words_per_thread = 2;        // CTAs per LL call = words / (threads * this); env RBX_LL_WPT (2 vs 4: 16 KB-256 KB 7-10 % faster at N=2, profiles/r02_ll_wpt_2gpu.jsonl)
   int ll_coresident = 0;              // co-resident CTAs of the LL kernel
   std::map<LLKey, std::unique_ptr<rbx::LLArgs>> ll_cache;  // per (buffers, count, dtype)
   // Launches of one communicator share a device epoch, so they must not overlap:
