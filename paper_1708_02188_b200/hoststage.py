@@ -91,8 +91,7 @@ class HostPipeline:
         for arr, _ in pairs:
             pin_array(arr)
             hosts.append(torch.from_numpy(arr))
-        windows = max(1, min(windows, n)) if n else 1
-        bounds = [(n * k // windows, n * (k + 1) // windows) for k in range(windows)]
+        bounds = window_bounds(n, windows)
         start = torch.cuda.Event()
         start.record(cur)
         for s in (self.s_in, self.s_red, self.s_out):
@@ -117,6 +116,24 @@ class HostPipeline:
         done.record(self.s_out)
         cur.wait_event(done)
         cur.synchronize()
+
+
+def window_bounds(n: int, windows: int) -> list:
+    """Element windows of the pipeline.  The first window's copy-in and the last
+    one's copy-out are the only transfers nothing overlaps, so from 6 windows up
+    the two ends are tapered (weights 1/4, 1/2, 1, ..., 1, 1/2, 1/4)."""
+    windows = max(1, min(windows, n)) if n else 1
+    if windows < 6:
+        w = [1.0] * windows
+    else:
+        w = [0.25, 0.5] + [1.0] * (windows - 4) + [0.5, 0.25]
+    total = sum(w)
+    edges, acc = [0], 0.0
+    for x in w:
+        acc += x
+        edges.append(int(round(n * acc / total)))
+    edges[-1] = n
+    return [(a, b) for a, b in zip(edges[:-1], edges[1:]) if b > a]
 
 
 def default_windows(nbytes: int, cap: int = 16) -> int:

@@ -5,7 +5,7 @@ the crash fraction of fault injection (the reference's crash_phase, runtime.py:
 import numpy as np
 import pytest
 
-from paper_1708_02188_b200.hoststage import default_windows
+from paper_1708_02188_b200.hoststage import default_windows, window_bounds
 from paper_1708_02188_b200.multiring import Grid
 from paper_1708_02188_b200.runtime import _crash_fraction, multiring_schedule
 
@@ -43,3 +43,14 @@ def test_host_dtype_table_covers_the_reference_dtypes():
     for dt in ("f32", "f64", "i64"):  # runtime.py:37
         assert dt in _NP_DTYPES.values()
     assert _NP_DTYPES[np.dtype(np.float32)] == "f32"
+
+
+@pytest.mark.parametrize("n,w", [(1, 8), (7, 3), (1000, 5), (102_400_000, 16), (25_600_000, 8), (13, 13)])
+def test_window_bounds_tile_the_buffer(n, w):
+    b = window_bounds(n, w)
+    assert b[0][0] == 0 and b[-1][1] == n
+    assert all(x[1] == y[0] for x, y in zip(b, b[1:]))
+    assert all(hi > lo for lo, hi in b)
+    if w >= 6 and n >= 1000:  # tapered ends: the unoverlapped first / last copies are the smallest
+        sizes = [hi - lo for lo, hi in b]
+        assert sizes[0] < sizes[1] < sizes[2] and sizes[-1] < sizes[-2] < sizes[-3]
