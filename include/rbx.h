@@ -111,8 +111,9 @@ int rbx_comm_inject_fault(rbx_comm_t *comm, double fraction);
  * signalled, 30 steps done, 31 exit.  Tracing / profiling subsystem. */
 int rbx_comm_trace(rbx_comm_t *comm, uint64_t *out, int cap);
 /* Page-lock host memory in place (PlacedBuffer(numpy) staging, hoststage.py): copies from / to it then
- * run at the host link's DMA rate.  Already-registered memory is not an error. */
-int rbx_host_register(void *ptr, size_t bytes);
+ * run at the host link's DMA rate.  Memory that is already page-locked is not an error; *registered
+ * (optional) is 1 only if this call registered it (then rbx_host_unregister releases it). */
+int rbx_host_register(void *ptr, size_t bytes, int *registered);
 int rbx_host_unregister(void *ptr);
 /* Diagnostic: a 1-thread kernel on `stream` that writes the device's %globaltimer (ns, the clock of
  * rbx_comm_trace) to the device word *dst -- brackets a collective on the device clock. */

@@ -76,7 +76,7 @@ def lib() -> ctypes.CDLL:
     _sig(L.rbx_comm_trace, c_int, _VP, ctypes.POINTER(ctypes.c_uint64), c_int)
     _sig(L.rbx_comm_inject_fault, c_int, _VP, ctypes.c_double)
     _sig(L.rbx_stamp, c_int, _VP, _VP)
-    _sig(L.rbx_host_register, c_int, _VP, c_size)
+    _sig(L.rbx_host_register, c_int, _VP, c_size, _INTP)
     _sig(L.rbx_host_unregister, c_int, _VP)
     _sig(L.rbx_fused_harness, c_int, _INTP, c_int, c_int, ctypes.POINTER(_VP), c_size, c_int, c_int, c_int, _VP)
     _sig(L.rbx_register_buffer, c_int, _VP, _VP, c_size, HP, ctypes.POINTER(ctypes.c_uint64), _INTP)

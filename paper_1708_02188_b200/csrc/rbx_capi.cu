@@ -1407,13 +1407,19 @@ int rbx_fused_harness(const int* dims, int ndims, int rank, void* const* bufs, s
   return RBX_OK;
 }
 
-int rbx_host_register(void* ptr, size_t bytes) {
+int rbx_host_register(void* ptr, size_t bytes, int* registered) {
+  if (registered) *registered = 0;
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, ptr) == cudaSuccess && attr.type == cudaMemoryTypeHost)
+    return RBX_OK;  // already page-locked (cudaHostAlloc / pinned allocator): nothing to do
+  (void)cudaGetLastError();
   const cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterDefault);
   if (e != cudaSuccess) {
     (void)cudaGetLastError();  // not sticky: do not leave it for the next caller's error check
     if (e == cudaErrorHostMemoryAlreadyRegistered) return RBX_OK;
     return fail(RBX_ERR_CUDA, std::string("cudaHostRegister: ") + cudaGetErrorString(e));
   }
+  if (registered) *registered = 1;
   return RBX_OK;
 }
 

@@ -56,8 +56,11 @@ def pin_array(arr: np.ndarray) -> None:
     if hit is not None:
         L.rbx_host_unregister(ctypes.c_void_p(addr))
         del _REGISTERED[addr]
-    if L.rbx_host_register(ctypes.c_void_p(addr), nbytes) != 0:
+    did = ctypes.c_int(0)
+    if L.rbx_host_register(ctypes.c_void_p(addr), nbytes, ctypes.byref(did)) != 0:
         return  # the copies still work, through the driver's pageable path
+    if not did.value:
+        return  # already page-locked memory (e.g. host_empty): not ours to release
     _REGISTERED[addr] = nbytes
 
     def _release(a=addr):
@@ -116,6 +119,17 @@ class HostPipeline:
         done.record(self.s_out)
         cur.wait_event(done)
         cur.synchronize()
+
+
+def host_empty(n: int, dtype: str = "f32") -> np.ndarray:
+    """A numpy array in page-locked memory from the CUDA host allocator (torch's pinned
+    pool).  Host buffers allocated this way cross PCIe ~13 % faster than malloc'd arrays
+    page-locked in place (49 vs 43 GB/s each way with both directions busy,
+    profiles/r02_hostmem_probe.jsonl)."""
+    torch = _torch()
+    tdt = {"f32": torch.float32, "f64": torch.float64, "i64": torch.int64, "i32": torch.int32,
+           "f16": torch.float16}[dtype]
+    return torch.empty(n, dtype=tdt, pin_memory=True).numpy()  # the array keeps the tensor alive
 
 
 def window_bounds(n: int, windows: int) -> list:

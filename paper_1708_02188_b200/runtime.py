@@ -42,6 +42,7 @@ DEFAULT_TIMEOUT_S = 30.0  # runtime.py:39
 
 __all__ = [
     "CollectiveError", "PlacedBuffer", "assign", "Workload", "generate_input", "RankResult", "LaunchReport",
+    "host_empty",
     "RankContext", "owned_region", "reduce_scatter", "allgather", "allreduce", "allreduce_buckets", "launch",
     "plan_fingerprint", "DTYPES",
 ]
@@ -51,6 +52,14 @@ def _torch():
     import torch
 
     return torch
+
+
+def host_empty(n: int, dtype: str = "f32"):
+    """numpy array in page-locked host memory for PlacedBuffer(memory="host"):
+    the fastest host buffers for the GPU path (hoststage.host_empty)."""
+    from .hoststage import host_empty as _he
+
+    return _he(n, dtype)
 
 
 def _dtype_name(t) -> str:
