@@ -94,6 +94,21 @@ def _main(rank, world, port, scenario, q):
                 q.put((rank, "ok", "no error"))
             except CollectiveError as exc:
                 q.put((rank, "ok", ("CollectiveError", str(exc))))
+        elif scenario == "host_pipeline":
+            # multi-window host path (hoststage: page-locked, 3 streams, tapered windows) on a
+            # malloc'd array and on a runtime.host_empty array; results vs the reference order
+            from oracle import ringbox_oracle as orc
+            from paper_1708_02188_b200.runtime import host_empty
+
+            n = 3_000_017  # 12 MB of f32: 11 windows, ragged
+            out = []
+            for kind in ("numpy", "host_empty"):
+                x = orc.generate_input(31, 0, rank, n, "f32")
+                arr = x.copy() if kind == "numpy" else host_empty(n, "f32")
+                arr[...] = x
+                allreduce(ctx, PlacedBuffer(arr, memory="host"))
+                out.append((kind, orc.sha256(arr)))
+            q.put((rank, "ok", out))
         elif scenario == "bytes_sent":
             buf = PlacedBuffer(np.arange(10, dtype=np.int64))
             allreduce(ctx, buf)
@@ -155,6 +170,20 @@ def test_allgather_broadcasts_owned_chunks(world):
 def test_length_mismatch_raises():
     for r, out in _run(2, "mismatch").items():
         assert out[0] == "CollectiveError", (r, out)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_host_buffer_pipeline_matches_reference(world):
+    """PlacedBuffer(memory="host") through the windowed host pipeline equals the
+    reference-order allreduce bit for bit, for plain and host_empty arrays."""
+    from oracle import ringbox_oracle as orc
+
+    n = 3_000_017
+    parts = [orc.generate_input(31, 0, r, n, "f32") for r in range(world)]
+    want = orc.sha256(orc.closed_form_allreduce(orc.Grid((world,)), parts))
+    for r, out in _run(world, "host_pipeline").items():
+        for kind, dig in out:
+            assert dig == want, (r, kind)
 
 
 def test_bytes_sent_counts_payload():
