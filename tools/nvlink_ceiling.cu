@@ -237,7 +237,9 @@ int main(int argc, char** argv) {
     for (int all = 0; all < 2; ++all) {
       const char* pat = all ? "bidi" : "1dir";
       // SM engines: grid x threads, U loads in flight
-      const int grids[] = {sms, 2 * sms, 4 * sms};
+      // PROBE_FEW_CTAS=1: small grids (how much one SM can move: collectives overlapping compute)
+      const bool few = std::getenv("PROBE_FEW_CTAS") != nullptr;
+      std::vector<int> grids = few ? std::vector<int>{16, 32, 64} : std::vector<int>{sms, 2 * sms, 4 * sms};
       for (int g : grids) {
         for (int mode = 0; mode < 3; ++mode) {  // 0 pull, 1 push, 2 mix
           const char* eng = mode == 0 ? "ldg" : mode == 1 ? "stg" : "mix";
@@ -257,7 +259,9 @@ int main(int argc, char** argv) {
       // TMA bulk
       for (int push = 0; push < 2; ++push) {
         struct BC { int tile, stages, grid; };
-        const BC bcs[] = {{16384, 8, sms}, {32768, 4, sms}, {65536, 3, sms}, {32768, 4, 2 * sms}};
+        std::vector<BC> bcs = few ? std::vector<BC>{{32768, 4, 16}, {65536, 3, 16}, {32768, 4, 32}, {65536, 3, 32},
+                                                    {32768, 4, 64}}
+                                  : std::vector<BC>{{16384, 8, sms}, {32768, 4, sms}, {65536, 3, sms}, {32768, 4, 2 * sms}};
         for (const BC& c : bcs) {
           float ms = time_it(all, [&](int d) {
             Pairs P = pairs(d, B, push, 1, 1);
