@@ -210,6 +210,7 @@ struct rbx_comm {
   bool plain_launch = false;  // env RBX_PLAIN_LAUNCH=1: fused kernel through cudaLaunchKernel (no launch attributes)
   bool rings_specialised = true;  // RING_DIMS through rbx_rings_kernel where possible; env RBX_RINGS_KERNEL=0: generic
   bool rings_gpu_fence = true;    // local-only stages signal after a GPU-scope fence; env RBX_RINGS_GPU_FENCE=0: sys release
+  bool push_specialised = true;   // MODE_PUSH allreduce through the matched-stage kernel; env RBX_PUSH_KERNEL=0: generic
 };
 
 namespace {
@@ -366,45 +367,61 @@ const void* rings_kernel_for(int dtype) {
   }
 }
 
-// Arguments of the RING_DIMS kernel from a RING_DIMS allreduce plan (rbx_plan.cpp):
-// steps 0..m-1 are the reduce-scatter stages, m..2m-2 the all-gathers, the last step
-// is the exit wait.  Every wait becomes a MATCHED wait (rbx_rings.cuh explains why that
-// is sufficient); slots are the step indices.  Ring sizes must be 2, 4 or 8.
+// Arguments of the matched-stage kernel (rbx_rings.cuh) from a RING_DIMS or PUSH allreduce
+// plan (rbx_plan.cpp): every plan step becomes one kernel stage per segment (a PUSH scatter
+// step has one segment per peer); the step's waits go to its first stage, its signals to its
+// last; slots are the plan's.  Every wait becomes a MATCHED wait (rbx_rings.cuh explains why
+// that is sufficient).  The last plan step is the exit wait.
 bool rings_args_from_plan(const rbx_comm* c, const rbx::Plan& p, const std::vector<void*>& table, rbx::RingsArgs* a) {
   std::memset(a, 0, sizeof(*a));
-  const int ns = p.nsteps - 1;  // data stages
-  if (ns < 3 || ns > RBX_RINGS_MAX_STAGES || p.steps[ns].nseg != 0) return false;
+  const int nsteps = p.nsteps - 1;  // data steps
+  if (nsteps < 1 || p.steps[nsteps].nseg != 0) return false;
   a->me = c->rank;
-  a->nstages = ns;
   a->my_sig = c->sig[c->rank];
   for (int q = 0; q < c->nranks; ++q) a->sig[q] = c->sig[q];
   a->nentry = p.nentry;
   for (int i = 0; i < p.nentry; ++i) a->entry_peer[i] = p.entry_peers[i];
-  for (int s = 0; s <= ns; ++s) {
+  int ns = 0;
+  for (int s = 0; s <= nsteps; ++s) {
     const rbx::Step& st = p.steps[s];
-    for (int w = 0; w < st.nwait; ++w)
-      if (p.waits[st.wait0 + w].slot != s) return false;
-    if (s == ns) {
+    for (int w = 1; w < st.nwait; ++w)
+      if (p.waits[st.wait0 + w].slot != p.waits[st.wait0].slot) return false;
+    if (s == nsteps) {
       a->nexit = st.nwait;
+      a->exit_slot = st.nwait ? p.waits[st.wait0].slot : 0;
       for (int w = 0; w < st.nwait; ++w) a->exit_peer[w] = p.waits[st.wait0 + w].peer;
       break;
     }
-    if (st.nseg != 1) return false;
-    const rbx::Seg& sg = p.segs[st.seg0];
-    if (sg.acc || sg.nlev != 1 || !(sg.nsrc == 1 || sg.nsrc == 2 || sg.nsrc == 4 || sg.nsrc == 8)) return false;
-    rbx::RingStage& R = a->st[s];
-    R.off = sg.off;
-    R.len = sg.len;
-    R.nsrc = sg.nsrc;
-    R.ndst = sg.ndst;
-    for (int j = 0; j < sg.nsrc; ++j) R.src[j] = static_cast<const char*>(table[sg.tbl + sg.src[j]]);
-    for (int d = 0; d < sg.ndst; ++d) R.dst[d] = static_cast<char*>(table[sg.tbl + sg.dst[d]]);
-    R.nwait = s == 0 ? 0 : (uint8_t)st.nwait;  // stage 0 waits on the entry flags
-    for (int w = 0; s > 0 && w < st.nwait; ++w) R.wait_peer[w] = p.waits[st.wait0 + w].peer;
-    R.nsig = (uint8_t)st.nsig;
-    R.local_only = (uint8_t)(c->rings_gpu_fence && sg.ndst == 1 && sg.dst[0] == c->rank);
-    for (int k = 0; k < st.nsig; ++k) R.sig_peer[k] = p.sigs[st.sig0 + k];
+    if (st.nseg < 1 || ns + st.nseg > RBX_RINGS_MAX_STAGES) return false;
+    for (int k = 0; k < st.nseg; ++k) {
+      const rbx::Seg& sg = p.segs[st.seg0 + k];
+      const bool shape_ok = (sg.nlev == 1 && (sg.nsrc == 1 || sg.nsrc == 2 || sg.nsrc == 4 || sg.nsrc == 8)) ||
+                            (sg.nlev == 2 && (sg.nsrc == 4 || sg.nsrc == 8)) || (sg.nlev == 3 && sg.nsrc == 8);
+      if (sg.acc || !shape_ok) return false;
+      rbx::RingStage& R = a->st[ns++];
+      R.off = sg.off;
+      R.len = sg.len;
+      R.nsrc = sg.nsrc;
+      R.ndst = sg.ndst;
+      R.nlev = sg.nlev;
+      for (int j = 0; j < sg.nsrc; ++j) {
+        R.src[j] = static_cast<const char*>(table[sg.tbl + sg.src[j]]);
+        R.ctrl[j] = sg.ctrl[j];
+      }
+      for (int d = 0; d < sg.ndst; ++d) R.dst[d] = static_cast<char*>(table[sg.tbl + sg.dst[d]]);
+      // stage 0 of a plan with an entry handshake waits on the entry flags instead
+      const bool first = k == 0 && !(s == 0 && p.nentry);
+      R.nwait = first ? (uint8_t)st.nwait : 0;
+      R.wait_slot = st.nwait ? p.waits[st.wait0].slot : 0;
+      for (int w = 0; first && w < st.nwait; ++w) R.wait_peer[w] = p.waits[st.wait0 + w].peer;
+      const bool last = k == st.nseg - 1;
+      R.nsig = last ? (uint8_t)st.nsig : 0;
+      R.sig_slot = (uint8_t)(s + 1);
+      for (int j = 0; last && j < st.nsig; ++j) R.sig_peer[j] = p.sigs[st.sig0 + j];
+      R.local_only = (uint8_t)(c->rings_gpu_fence && sg.ndst == 1 && sg.dst[0] == c->rank);
+    }
   }
+  a->nstages = ns;
   return true;
 }
 
@@ -517,6 +534,7 @@ int common_init(rbx_comm* c, const int* dims, int ndims, int device, int threads
   if (const char* t = std::getenv("RBX_PLAIN_LAUNCH")) c->plain_launch = std::atoi(t) != 0;
   if (const char* t = std::getenv("RBX_RINGS_KERNEL")) c->rings_specialised = std::atoi(t) != 0;
   if (const char* t = std::getenv("RBX_RINGS_GPU_FENCE")) c->rings_gpu_fence = std::atoi(t) != 0;
+  if (const char* t = std::getenv("RBX_PUSH_KERNEL")) c->push_specialised = std::atoi(t) != 0;
   if (const char* t = std::getenv("RBX_LOCAL_CTAS_PER_SM")) c->local_ctas_per_sm = std::atoi(t);
   if (const char* t = std::getenv("RBX_BYTES_PER_CTA")) c->bytes_per_cta = (size_t)std::max(1L, std::atol(t));
   if (const char* t = std::getenv("RBX_MIN_BLOCKS")) c->min_blocks = std::max(1, std::atoi(t));
@@ -1054,8 +1072,8 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
     }
     // the paper's per-dimension rings through the specialised kernel: whole aligned buffer,
     // 4/8-byte types (16-bit types keep fp32 stage partials in workspaces: generic kernel)
-    if (mode == RBX_MODE_RING_DIMS && op == RBX_OP_ALLREDUCE && !one_ring && !ws && nbufs == 1 && whole &&
-        spec.mis == 0 && c->rings_specialised) {
+    const bool matched_stages = (mode == RBX_MODE_RING_DIMS && !one_ring && !ws) || (push && c->push_specialised);
+    if (matched_stages && op == RBX_OP_ALLREDUCE && nbufs == 1 && whole && spec.mis == 0 && c->rings_specialised) {
       const void* fn = rings_kernel_for(dtype);
       int per_sm = 0;
       if (fn) RBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, c->threads, 0));

@@ -25,12 +25,20 @@
 // every peer, by the CTA with the same index -- so each dependency is a
 // MATCHED wait on one flag per (peer, CTA) instead of an ALL-CTA barrier
 // (the generic step interpreter's RING_DIMS pays one ALL barrier per stage).
+//
+// The same engine runs MODE_PUSH (two-shot, NVLink writes only): one stage per
+// peer scatters this rank's input of that peer's owned region into the peer's
+// inbox, then one stage folds the owned region from the own buffer and the
+// inbox slots in the nested reference order and pushes the result into every
+// buffer.  Posted writes need no round trip, so with few SMs (a collective
+// overlapping compute) pushes move 1.5-2x the bytes per SM that pulls do
+// (profiles/r02_nvlink_few_ctas_2gpu.jsonl).
 #pragma once
 #include "rbx_fused.cuh"
 
 namespace rbx {
 
-#define RBX_RINGS_MAX_STAGES (2 * RBX_MAX_LEVELS - 1)
+#define RBX_RINGS_MAX_STAGES 9  // RING_DIMS: 2m-1 <= 7; PUSH: N-1 scatter stages + 1 fold (N <= 8)
 
 struct RingStage {
   int64_t off, len;                 // element region of the stage
@@ -38,12 +46,16 @@ struct RingStage {
   char* dst[RBX_MAX_RANKS];         // RS: {my buffer}, last RS: ring members (rotated); AG: other ring members
   uint8_t nsrc, ndst, nwait, nsig;
   uint8_t local_only;               // every destination is this rank's own buffer (see the release below)
-  uint8_t wait_peer[RBX_MAX_RANKS]; // matched waits before the stage (slot = stage index)
-  uint8_t sig_peer[RBX_MAX_RANKS];  // matched release signals after it (slot = stage index + 1)
+  uint8_t nlev;                     // nesting depth of the fold (1: one ring; PUSH folds all dims at once)
+  uint8_t wait_slot, sig_slot;      // flag slots of the stage's waits and signals
+  uint8_t wait_peer[RBX_MAX_RANKS]; // matched waits before the stage
+  uint8_t sig_peer[RBX_MAX_RANKS];  // matched release signals after it
+  uint8_t ctrl[RBX_MAX_RANKS];      // nested-fold control per operand (rbx::fold_ctrl)
 };
 
 struct RingsArgs {
   int me, nstages, nentry, nexit;
+  int exit_slot;
   uint32_t* my_sig;
   uint32_t* sig[RBX_MAX_RANKS];     // every rank's signal area (mapped)
   uint8_t entry_peer[RBX_MAX_RANKS];
@@ -64,7 +76,7 @@ constexpr int kRingTileVec = 128;
 
 // One warp folds NSRC operands (single ring level) over vectors [v0, v1) (at most
 // one tile), 8 loads in flight per lane; NSRC == 1 is the all-gather copy.
-template <typename T, int NSRC>
+template <typename T, int NSRC, int NLEV>
 __device__ __forceinline__ void ring_tile(const RingStage& S, int64_t v0, int64_t v1, int lane) {
   constexpr int VEC = Traits<T>::VEC;
   constexpr int U = NSRC >= 8 ? 1 : (8 / NSRC > 4 ? 4 : 8 / NSRC);
@@ -83,13 +95,13 @@ __device__ __forceinline__ void ring_tile(const RingStage& S, int64_t v0, int64_
       if (NSRC == 1) {
         out = raw[u][0];
       } else {
-        FoldState<T, VEC, 1> f;
+        FoldState<T, VEC, NLEV> f;
 #pragma unroll
         for (int j = 0; j < NSRC; ++j) {
           typename Traits<T>::Acc x[VEC];
 #pragma unroll
           for (int l = 0; l < VEC; ++l) x[l] = Traits<T>::lane(raw[u][j], l);
-          f.feed(j == 0 ? 1u : 0u, x);  // the first operand starts the (only) level
+          f.feed(S.ctrl[j], x);
         }
         out = pack_result(f);
       }
@@ -99,7 +111,7 @@ __device__ __forceinline__ void ring_tile(const RingStage& S, int64_t v0, int64_
   }
 }
 
-template <typename T, int NSRC>
+template <typename T, int NSRC, int NLEV>
 __device__ __forceinline__ void ring_scalar(const RingStage& S, int64_t e) {
   using Tr = Traits<T>;
   using Bt = typename Tr::Bits;
@@ -108,11 +120,11 @@ __device__ __forceinline__ void ring_scalar(const RingStage& S, int64_t e) {
   if (NSRC == 1) {
     out = __ldcg(reinterpret_cast<const Bt*>(S.src[0] + byte));
   } else {
-    FoldState<T, 1, 1> f;
+    FoldState<T, 1, NLEV> f;
 #pragma unroll
     for (int j = 0; j < NSRC; ++j) {
       typename Tr::Acc x[1] = {Tr::from_bits(__ldcg(reinterpret_cast<const Bt*>(S.src[j] + byte)))};
-      f.feed(j == 0 ? 1u : 0u, x);
+      f.feed(S.ctrl[j], x);
     }
     out = Tr::to_bits(f.result(0));
   }
@@ -121,7 +133,7 @@ __device__ __forceinline__ void ring_scalar(const RingStage& S, int64_t e) {
 
 // CTA b's share of one stage: its warps walk the tiles they own inside the region.
 // tlimit >= 0 (fault injection): at most that many tiles per warp.
-template <typename T, int NSRC>
+template <typename T, int NSRC, int NLEV>
 __device__ void ring_stage(const RingStage& S, int b, int nb, int64_t tlimit) {
   constexpr int VEC = Traits<T>::VEC;
   constexpr int64_t TE = (int64_t)kRingTileVec * VEC;  // elements per tile
@@ -139,11 +151,11 @@ __device__ void ring_stage(const RingStage& S, int b, int nb, int64_t tlimit) {
     const int64_t a0 = k * TE > e0 ? k * TE : e0, a1 = (k + 1) * TE < e1 ? (k + 1) * TE : e1;
     const int64_t v0 = (a0 + VEC - 1) / VEC, v1 = a1 / VEC;  // whole vectors inside [a0, a1)
     if (v0 < v1) {
-      ring_tile<T, NSRC>(S, v0, v1, lane);
-      for (int64_t e = a0 + lane; e < v0 * VEC; e += 32) ring_scalar<T, NSRC>(S, e);
-      for (int64_t e = v1 * VEC + lane; e < a1; e += 32) ring_scalar<T, NSRC>(S, e);
+      ring_tile<T, NSRC, NLEV>(S, v0, v1, lane);
+      for (int64_t e = a0 + lane; e < v0 * VEC; e += 32) ring_scalar<T, NSRC, NLEV>(S, e);
+      for (int64_t e = v1 * VEC + lane; e < a1; e += 32) ring_scalar<T, NSRC, NLEV>(S, e);
     } else {
-      for (int64_t e = a0 + lane; e < a1; e += 32) ring_scalar<T, NSRC>(S, e);
+      for (int64_t e = a0 + lane; e < a1; e += 32) ring_scalar<T, NSRC, NLEV>(S, e);
     }
   }
 }
@@ -151,11 +163,14 @@ __device__ void ring_stage(const RingStage& S, int b, int nb, int64_t tlimit) {
 template <typename T>
 __device__ __forceinline__ void ring_stage_dispatch(const RingsArgs& a, const RingStage& S, int b, int nb,
                                                     int64_t tlimit) {
-  switch (S.nsrc) {
-    case 1: ring_stage<T, 1>(S, b, nb, tlimit); break;
-    case 2: ring_stage<T, 2>(S, b, nb, tlimit); break;
-    case 4: ring_stage<T, 4>(S, b, nb, tlimit); break;
-    case 8: ring_stage<T, 8>(S, b, nb, tlimit); break;
+  switch (S.nsrc * 8 + S.nlev) {
+    case 1 * 8 + 1: ring_stage<T, 1, 1>(S, b, nb, tlimit); break;
+    case 2 * 8 + 1: ring_stage<T, 2, 1>(S, b, nb, tlimit); break;
+    case 4 * 8 + 1: ring_stage<T, 4, 1>(S, b, nb, tlimit); break;
+    case 8 * 8 + 1: ring_stage<T, 8, 1>(S, b, nb, tlimit); break;
+    case 4 * 8 + 2: ring_stage<T, 4, 2>(S, b, nb, tlimit); break;  // PUSH over (2,2)
+    case 8 * 8 + 2: ring_stage<T, 8, 2>(S, b, nb, tlimit); break;  // PUSH over (2,4) / (4,2)
+    case 8 * 8 + 3: ring_stage<T, 8, 3>(S, b, nb, tlimit); break;  // PUSH over (2,2,2)
     default: break;
   }
 }
@@ -200,14 +215,15 @@ __global__ void __launch_bounds__(512, 1) rbx_rings_kernel(const __grid_constant
   __syncthreads();
   const uint32_t e = s_epoch;
   const uint64_t t0 = global_ns();
-  // ENTRY (slot 0): every ring partner's inputs are ready (relaxed: nothing written yet)
+  // ENTRY (slot 0): every ring partner's inputs are ready (relaxed: nothing written yet).
+  // PUSH has none: no peer ever reads this rank's buffer (see rbx_plan.cpp MODE_PUSH)
   if ((int)threadIdx.x < a.nentry) st_relaxed_sys(a.sig[a.entry_peer[threadIdx.x]] + flag_index(0, a.me, b), e);
-  if (!rings_wait(a, a.nentry, a.entry_peer, 0, b, e, t0, abort_word, &s_fail)) return;
+  if (a.nentry && !rings_wait(a, a.nentry, a.entry_peer, 0, b, e, t0, abort_word, &s_fail)) return;
   if (tr) tr[2] = global_ns();
   pdl_launch_dependents();
   for (int s = 0; s < a.nstages; ++s) {
     const RingStage& S = a.st[s];
-    if (s > 0 && !rings_wait(a, S.nwait, S.wait_peer, s, b, e, t0, abort_word, &s_fail)) return;
+    if (S.nwait && !rings_wait(a, S.nwait, S.wait_peer, S.wait_slot, b, e, t0, abort_word, &s_fail)) return;
     if (tr && s < 9) tr[3 + 3 * s] = global_ns();
     if (s == 0 && a.fault_milli >= 0) {  // injected crash: part of stage 0, then die without signalling
       const int64_t per_warp = S.len / ((int64_t)kRingTileVec * Traits<T>::VEC) / ((int64_t)nb * (blockDim.x / 32)) + 1;
@@ -218,7 +234,7 @@ __global__ void __launch_bounds__(512, 1) rbx_rings_kernel(const __grid_constant
     if (tr && s < 9) tr[4 + 3 * s] = global_ns();
     __syncthreads();  // the release is cumulative over the CTA's writes ordered by bar.sync
     if ((int)threadIdx.x < S.nsig) {
-      uint32_t* f = a.sig[S.sig_peer[threadIdx.x]] + flag_index(s + 1, a.me, b);
+      uint32_t* f = a.sig[S.sig_peer[threadIdx.x]] + flag_index(S.sig_slot, a.me, b);
       if (S.local_only) {
         // the stage wrote only this GPU's memory, which peers read through this GPU's L2:
         // a GPU-scope fence puts the writes there before the flag leaves (0.45 us instead
@@ -233,7 +249,7 @@ __global__ void __launch_bounds__(512, 1) rbx_rings_kernel(const __grid_constant
   }
   // EXIT: the last all-gather pushes into me have landed (earlier levels were waited on by
   // the stage that forwarded them), and transitively every partner is done reading me
-  if (!rings_wait(a, a.nexit, a.exit_peer, a.nstages, b, e, t0, abort_word, &s_fail)) return;
+  if (!rings_wait(a, a.nexit, a.exit_peer, a.exit_slot, b, e, t0, abort_word, &s_fail)) return;
   if (tr) tr[30] = global_ns();
   if (threadIdx.x == 0) {
     unsigned int* done = reinterpret_cast<unsigned int*>(my_sig + SigLayout::epoch_off + 1);
