@@ -393,6 +393,10 @@ bool rings_args_from_plan(const rbx_comm* c, const rbx::Plan& p, const std::vect
       break;
     }
     if (st.nseg < 1 || ns + st.nseg > RBX_RINGS_MAX_STAGES) return false;
+    if (st.nseg > 1 && a->group_count == 0) {  // one step, several segments: independent stages
+      a->group_first = ns;
+      a->group_count = st.nseg;
+    }
     for (int k = 0; k < st.nseg; ++k) {
       const rbx::Seg& sg = p.segs[st.seg0 + k];
       const bool shape_ok = (sg.nlev == 1 && (sg.nsrc == 1 || sg.nsrc == 2 || sg.nsrc == 4 || sg.nsrc == 8)) ||

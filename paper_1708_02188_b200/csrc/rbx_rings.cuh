@@ -56,6 +56,7 @@ struct RingStage {
 struct RingsArgs {
   int me, nstages, nentry, nexit;
   int exit_slot;
+  int group_first, group_count;     // stages [first, first+count) may run in any order (PUSH scatter)
   uint32_t* my_sig;
   uint32_t* sig[RBX_MAX_RANKS];     // every rank's signal area (mapped)
   uint8_t entry_peer[RBX_MAX_RANKS];
@@ -230,12 +231,23 @@ __global__ void __launch_bounds__(512, 1) rbx_rings_kernel(const __grid_constant
       ring_stage_dispatch<T>(a, S, b, nb, per_warp * a.fault_milli / 1000);
       return;
     }
-    ring_stage_dispatch<T>(a, S, b, nb, -1);
+    int last = s;
+    if (s == a.group_first && a.group_count > 1) {
+      // a group of independent stages (PUSH: the scatter into every peer's inbox): no
+      // waits between them and only the last one signals, so each CTA runs them in its
+      // own rotation and at any moment the GPU's pushes go to every peer, not to one
+      last = s + a.group_count - 1;
+      for (int i = 0; i < a.group_count; ++i) ring_stage_dispatch<T>(a, a.st[s + (i + b) % a.group_count], b, nb, -1);
+      s = last;
+    } else {
+      ring_stage_dispatch<T>(a, S, b, nb, -1);
+    }
+    const RingStage& L = a.st[last];
     if (tr && s < 9) tr[4 + 3 * s] = global_ns();
     __syncthreads();  // the release is cumulative over the CTA's writes ordered by bar.sync
-    if ((int)threadIdx.x < S.nsig) {
-      uint32_t* f = a.sig[S.sig_peer[threadIdx.x]] + flag_index(S.sig_slot, a.me, b);
-      if (S.local_only) {
+    if ((int)threadIdx.x < L.nsig) {
+      uint32_t* f = a.sig[L.sig_peer[threadIdx.x]] + flag_index(L.sig_slot, a.me, b);
+      if (L.local_only) {
         // the stage wrote only this GPU's memory, which peers read through this GPU's L2:
         // a GPU-scope fence puts the writes there before the flag leaves (0.45 us instead
         // of the 3.7 us system-scope release that has to drain NVLink pushes)
