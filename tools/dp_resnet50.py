@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--nblocks", type=int, default=32, help="CTAs per allreduce (SMs left to backward)")
+    ap.add_argument("--mode", default="auto", help="multi-ring mode (auto = fused; push: writes only, fewer SMs)")
     ap.add_argument("--t1-ms", type=float, default=None, help="N=1 step time for efficiency/overhead")
     args = ap.parse_args()
     import torch
@@ -59,7 +60,8 @@ def main():
         if args.comm == "multiring":
             dims = {2: (2,), 4: (2, 2), 8: (2, 2, 2)}.get(world, (world,))
             gloo = dist.new_group(backend="gloo")
-            ctx = RankContext(rank, Grid(dims), group=gloo, device=local, nblocks=args.nblocks, blocking=False)
+            ctx = RankContext(rank, Grid(dims), group=gloo, device=local, nblocks=args.nblocks, blocking=False,
+                              mode=args.mode)
         dp = MultiringDataParallel(model, ctx, comm=args.comm)
     opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9, foreach=True)
     torch.manual_seed(1 + rank)
@@ -122,6 +124,7 @@ def main():
             "engine": "MultiringDataParallel" if dp is not None else "single GPU",
             "comm": args.comm, "graph": bool(args.graph), "n_gpus": world, "batch_per_gpu": args.batch,
             "nblocks": args.nblocks if args.comm == "multiring" else None, "params": nparams,
+            "mode": args.mode if args.comm == "multiring" else None,
             "grad_bytes": nparams * 4, "buckets": len(dp.buckets) if dp is not None else None,
             "t_iter_ms": round(t_ms, 3), "images_per_s": round(world * args.batch / t_ms * 1e3, 1),
             "loss": float(loss_buf.item()),
