@@ -53,9 +53,10 @@ __device__ __forceinline__ unsigned ld_acq_sys(const unsigned* p) {
 // 10 pull `bytes` from the peer, store locally, relaxed.sys store to LOCAL flag
 // 11 one relaxed.sys store per CTA to LOCAL memory
 __global__ void __launch_bounds__(512) probe(int variant, unsigned* remote, unsigned* local, const int4* src,
-                                             int4* dst, long n16, unsigned e) {
+                                             int4* dst, long n16, unsigned e, int active) {
   const int b = blockIdx.x;
   __shared__ unsigned s;
+  if (variant >= 1 && variant <= 4 && b >= active) return;  // only the first `active` CTAs touch the peer
   if (variant == 1) {
     if (threadIdx.x == 0) st_rlx_sys(remote + b * 32, e);
   } else if (variant == 2) {
@@ -122,18 +123,19 @@ int main(int argc, char** argv) {
   unsigned e = 1;
   for (int grid : {148, 296}) {
     for (int v = 0; v < nvar; ++v) {
-      for (long bytes : sizes) {
+      for (long bytes : sizes) for (int act : {1, 4, 16, 64, 148, 296}) {
         const bool data = v == 6 || v == 7 || v == 8 || v == 10;
         if (!data && bytes != sizes[0]) continue;
+        if (act > grid || ((v < 1 || v > 4) && act != grid) || (v >= 3 && v <= 4 && act != grid)) continue;
         const int4* src = v == 6 || v == 10 ? rbuf : lbuf;
         int4* dst = v == 7 ? rbuf : lbuf2;
         const long n16 = bytes / 16;
-        for (int w = 0; w < 20; ++w) probe<<<grid, 512, 0, st>>>(v, remote, local, src, dst, n16, e++);
+        for (int w = 0; w < 20; ++w) probe<<<grid, 512, 0, st>>>(v, remote, local, src, dst, n16, e++, act);
         CK(cudaStreamSynchronize(st));
         std::vector<float> one;
         for (int i = 0; i < 200; ++i) {
           CK(cudaEventRecord(a, st));
-          probe<<<grid, 512, 0, st>>>(v, remote, local, src, dst, n16, e++);
+          probe<<<grid, 512, 0, st>>>(v, remote, local, src, dst, n16, e++, act);
           CK(cudaEventRecord(z, st));
           CK(cudaEventSynchronize(z));
           float ms;
@@ -142,15 +144,15 @@ int main(int argc, char** argv) {
         }
         std::sort(one.begin(), one.end());
         CK(cudaEventRecord(a, st));
-        for (int i = 0; i < 200; ++i) probe<<<grid, 512, 0, st>>>(v, remote, local, src, dst, n16, e++);
+        for (int i = 0; i < 200; ++i) probe<<<grid, 512, 0, st>>>(v, remote, local, src, dst, n16, e++, act);
         CK(cudaEventRecord(z, st));
         CK(cudaEventSynchronize(z));
         float ms;
         CK(cudaEventElapsedTime(&ms, a, z));
         std::printf(
-            "{\"grid\": %d, \"variant\": %d, \"what\": \"%s\", \"bytes\": %ld, \"single_us_p50\": %.2f, "
+            "{\"grid\": %d, \"active\": %d, \"variant\": %d, \"what\": \"%s\", \"bytes\": %ld, \"single_us_p50\": %.2f, "
             "\"single_us_p10\": %.2f, \"b2b_us\": %.2f}\n",
-            grid, v, names[v], data ? bytes : 0, one[one.size() / 2], one[one.size() / 10], ms * 1e3f / 200);
+            grid, act, v, names[v], data ? bytes : 0, one[one.size() / 2], one[one.size() / 10], ms * 1e3f / 200);
         std::fflush(stdout);
       }
     }
