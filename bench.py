@@ -63,11 +63,11 @@ def parse_args():
     p.add_argument("--no-nccl", action="store_true")
     p.add_argument("--curve", type=int, default=1, help="N>1: add busbw at 4 KB..1 GiB to the line")
     p.add_argument("--e2e-chunks", type=int, default=None,
-                   help="N=1: pipeline windows of the host-buffer e2e leg (default 8, best measured against the "
-                        "host PCIe ceiling, profiles/r01_pcie_probe_*gpu.jsonl); N>1 uses the runtime's default")
+                   help="N=1: pipeline windows of the host-buffer e2e leg (default 12, best measured against the "
+                        "host PCIe ceiling, profiles/r02_e2e_probe_align_1gpu.jsonl); N>1 uses the runtime's default")
     a = p.parse_args()
     if a.e2e_chunks is None:
-        a.e2e_chunks = 8 if a.gpus == 1 else 32
+        a.e2e_chunks = 12 if a.gpus == 1 else 32
     return a
 
 

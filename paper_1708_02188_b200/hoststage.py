@@ -74,50 +74,77 @@ def pin_array(arr: np.ndarray) -> None:
 
 
 class HostPipeline:
-    """Three streams (copy-in, reduce, copy-out) of one device."""
+    """Copy-in lanes, one reduce stream, copy-out lanes, of one device.
 
-    def __init__(self, device):
+    `lanes` copy streams per direction: each window's copies are dealt over
+    them (whole ranks when there are at least `lanes` buffers, otherwise
+    sub-ranges of the window), so several copy engines share each direction
+    of the host link."""
+
+    def __init__(self, device, lanes: int = 1):
         torch = _torch()
         self.device = device
+        self.lanes = max(1, int(lanes))
         with torch.cuda.device(device):
-            self.s_in, self.s_red, self.s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+            self.s_in = [torch.cuda.Stream() for _ in range(self.lanes)]
+            self.s_out = [torch.cuda.Stream() for _ in range(self.lanes)]
+            self.s_red = torch.cuda.Stream()
 
-    def run(self, pairs, n: int, windows: int, reduce) -> None:
+    def _pieces(self, hosts, devs, lo, hi):
+        """[(lane, host slice, device slice)] covering [lo, hi) of every buffer."""
+        L = self.lanes
+        parts = max(1, -(-L // len(hosts)))  # sub-ranges per buffer
+        out, k = [], 0
+        for h, d in zip(hosts, devs):
+            for a, b in window_bounds(hi - lo, parts, taper=False):
+                out.append((k % L, h[lo + a:lo + b], d[lo + a:lo + b]))
+                k += 1
+        return out
+
+    def run(self, pairs, n: int, windows: int, reduce, taper: bool = False, align_bytes: int = 1 << 16) -> None:
         """pairs: [(host numpy array, device tensor)], every array n elements.
         reduce(lo, hi, stream): enqueue the collective of window [lo, hi).
         Enqueued after the caller's current stream; the current stream waits
         for the last copy-out, then the host waits for it (the result is in
-        the numpy arrays when this returns)."""
+        the numpy arrays when this returns).  Equal windows with 64 KB-aligned
+        edges and one copy lane per direction measured best (N=1, 8 x 102.4 MB:
+        18.6 ms vs 21.7 ms for tapered, unaligned windows; 2 or 4 lanes per
+        direction 24-28 ms; profiles/r02_e2e_probe_*_1gpu.jsonl)."""
         torch = _torch()
         cur = torch.cuda.current_stream(self.device)
         hosts = []
         for arr, _ in pairs:
             pin_array(arr)
             hosts.append(torch.from_numpy(arr))
-        bounds = window_bounds(n, windows)
+        devs = [d for _, d in pairs]
+        align = max(1, align_bytes // max(1, hosts[0].element_size())) if hosts else 1
         start = torch.cuda.Event()
         start.record(cur)
-        for s in (self.s_in, self.s_red, self.s_out):
+        for s in self.s_in + self.s_out + [self.s_red]:
             s.wait_event(start)
-        for lo, hi in bounds:
-            if hi <= lo:
-                continue
-            with torch.cuda.stream(self.s_in):
-                for h, (_, d) in zip(hosts, pairs):
-                    d[lo:hi].copy_(h[lo:hi], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(self.s_in)
-            self.s_red.wait_event(ev)
+        for lo, hi in window_bounds(n, windows, taper=taper, align=align):
+            pieces = self._pieces(hosts, devs, lo, hi)
+            for j, s in enumerate(self.s_in):
+                with torch.cuda.stream(s):
+                    for lane, h, d in pieces:
+                        if lane == j:
+                            d.copy_(h, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(s)
+                self.s_red.wait_event(ev)
             reduce(lo, hi, self.s_red)
             ev = torch.cuda.Event()
             ev.record(self.s_red)
-            self.s_out.wait_event(ev)
-            with torch.cuda.stream(self.s_out):
-                for h, (_, d) in zip(hosts, pairs):
-                    h[lo:hi].copy_(d[lo:hi], non_blocking=True)
-        done = torch.cuda.Event()
-        done.record(self.s_out)
-        cur.wait_event(done)
+            for j, s in enumerate(self.s_out):
+                s.wait_event(ev)
+                with torch.cuda.stream(s):
+                    for lane, h, d in pieces:
+                        if lane == j:
+                            h.copy_(d, non_blocking=True)
+        for s in self.s_out:
+            done = torch.cuda.Event()
+            done.record(s)
+            cur.wait_event(done)
         cur.synchronize()
 
 
@@ -132,12 +159,15 @@ def host_empty(n: int, dtype: str = "f32") -> np.ndarray:
     return torch.empty(n, dtype=tdt, pin_memory=True).numpy()  # the array keeps the tensor alive
 
 
-def window_bounds(n: int, windows: int) -> list:
+def window_bounds(n: int, windows: int, taper: bool = True, align: int = 1) -> list:
     """Element windows of the pipeline.  The first window's copy-in and the last
     one's copy-out are the only transfers nothing overlaps, so from 6 windows up
-    the two ends are tapered (weights 1/4, 1/2, 1, ..., 1, 1/2, 1/4)."""
+    the two ends are tapered (weights 1/4, 1/2, 1, ..., 1, 1/2, 1/4) unless
+    `taper` is false.  Inner edges are rounded to multiples of `align` elements:
+    host<->device copies that start or end off a 64 KB boundary run measurably
+    slower (profiles/r02_e2e_probe_1gpu.jsonl)."""
     windows = max(1, min(windows, n)) if n else 1
-    if windows < 6:
+    if windows < 6 or not taper:
         w = [1.0] * windows
     else:
         w = [0.25, 0.5] + [1.0] * (windows - 4) + [0.5, 0.25]
@@ -145,14 +175,17 @@ def window_bounds(n: int, windows: int) -> list:
     edges, acc = [0], 0.0
     for x in w:
         acc += x
-        edges.append(int(round(n * acc / total)))
+        e = int(round(n * acc / total))
+        if align > 1:
+            e = int(round(e / align)) * align
+        edges.append(min(e, n))
     edges[-1] = n
     return [(a, b) for a, b in zip(edges[:-1], edges[1:]) if b > a]
 
 
 def default_windows(nbytes: int, cap: int = 16) -> int:
-    """Pipeline depth: ~1 window per MiB up to `cap` (for a 102.4 MB buffer at N=2,
-    8 / 16 / 64 windows reach 0.948 / 0.956 / 0.890 of the host link measured in the
-    same run, profiles/r02_host_windows_2gpu.jsonl); small buffers stay one window
-    (one launch, the LL kernel when it qualifies)."""
+    """Pipeline depth: ~1 window per MiB up to `cap` (one 102.4 MB buffer: 12 / 16
+    equal 64 KB-aligned windows reach 0.89 / 0.89 of the host link measured in the
+    same run, 4 windows 0.81, profiles/r02_e2e_probe_align_1gpu.jsonl); small
+    buffers stay one window (one launch, the LL kernel when it qualifies)."""
     return max(1, min(cap, nbytes >> 20))

@@ -99,7 +99,7 @@ class VirtualRanks:
         devs = staging[key]
         if getattr(self, "_pipe", None) is None:
             self._pipe = HostPipeline(self.device)
-        w = windows or default_windows(arrays[0].nbytes * self.nranks, cap=8)
+        w = windows or default_windows(arrays[0].nbytes * self.nranks, cap=12)
         self._pipe.run(list(zip(arrays, devs)), n, w,
                        lambda lo, hi, s: self.collective(devs, mode=mode, stream=s, window=(lo, hi)))
         self.check()

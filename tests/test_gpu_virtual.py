@@ -331,3 +331,32 @@ def test_windows_compose_to_the_full_allreduce(mode):
         for t in ts:
             assert np.array_equal(t.cpu().numpy(), want)
         vr.close()
+
+
+@pytest.mark.parametrize("windows", [1, 5, 12])
+@pytest.mark.parametrize("n", [1, 4099, 1_000_003])
+def test_allreduce_host_pipeline_bit_exact(n, windows):
+    """VirtualRanks.allreduce_host (the bench's N=1 e2e call): page-locked numpy
+    buffers streamed through equal, 64 KB-aligned windows on three streams;
+    every window is a full-geometry allreduce of its elements, so the result
+    equals the reference order over the whole buffer."""
+    _torch()
+    from paper_1708_02188_b200.runtime import host_empty
+    from paper_1708_02188_b200.virtual import VirtualRanks
+
+    dims = (2, 2, 2)
+    grid = orc.Grid(dims)
+    parts = [orc.generate_input(0, 0, r, n, "f32") for r in range(8)]
+    want = orc.closed_form_allreduce(grid, parts)
+    vr = VirtualRanks(dims, device=0, nblocks_per_rank=0)
+    try:
+        for kind in ("numpy", "host_empty"):
+            arrays = [p.copy() if kind == "numpy" else host_empty(n, "f32") for p in parts]
+            if kind == "host_empty":
+                for a, p in zip(arrays, parts):
+                    a[...] = p
+            vr.allreduce_host(arrays, mode="local", windows=windows)
+            for a in arrays:
+                assert np.array_equal(a, want), (kind, n, windows)
+    finally:
+        vr.close()

@@ -54,3 +54,24 @@ def test_window_bounds_tile_the_buffer(n, w):
     if w >= 6 and n >= 1000:  # tapered ends: the unoverlapped first / last copies are the smallest
         sizes = [hi - lo for lo, hi in b]
         assert sizes[0] < sizes[1] < sizes[2] and sizes[-1] < sizes[-2] < sizes[-3]
+
+
+@pytest.mark.parametrize("nbuf,lanes", [(1, 1), (1, 2), (1, 4), (8, 1), (8, 2), (8, 4), (3, 4), (2, 3)])
+def test_pipeline_lanes_cover_every_window_once(nbuf, lanes):
+    import torch
+
+    from paper_1708_02188_b200.hoststage import HostPipeline
+
+    pipe = HostPipeline.__new__(HostPipeline)  # no CUDA streams needed for the split
+    pipe.lanes = lanes
+    n = 1001
+    hosts = [torch.zeros(n, dtype=torch.int32) for _ in range(nbuf)]
+    devs = [torch.zeros(n, dtype=torch.int32) for _ in range(nbuf)]
+    for lo, hi in window_bounds(n, 7, taper=False):
+        pieces = pipe._pieces(hosts, devs, lo, hi)
+        assert {lane for lane, _, _ in pieces} == set(range(min(lanes, len(pieces))))
+        for _, h, d in pieces:
+            h += 1
+            d += 1
+    for t in hosts + devs:
+        assert torch.equal(t, torch.ones(n, dtype=torch.int32))  # every element in exactly one piece

@@ -8,8 +8,9 @@ same bytes as bench.py's N=1 e2e leg.  Prints one JSON line per measurement
   link_bidi     H2D and D2H of every array at once on two streams (bench.py host_link_ms)
   h2d / d2h     one direction alone, one stream
   h2d_2s        one direction alone, arrays split over two streams
-  copy_pipe     HostPipeline with a no-op reduce: the copies' window structure alone
-  e2e           VirtualRanks.allreduce_host (the bench's e2e call)
+  copy_pipe     HostPipeline(lanes) with a no-op reduce: the copies' window structure alone
+  pipe          HostPipeline(lanes) with the local-reduce kernel per window
+  e2e           VirtualRanks.allreduce_host (the bench's e2e call, its default pipeline)
 """
 
 import argparse
@@ -27,7 +28,9 @@ def main():
     ap.add_argument("--ranks", type=int, default=8)
     ap.add_argument("--n", type=int, default=25_600_000)
     ap.add_argument("--iters", type=int, default=5)
-    ap.add_argument("--windows", default="4,8,12,16")
+    ap.add_argument("--windows", default="2,3,4,6,8,12,16")
+    ap.add_argument("--lanes", default="1")
+    ap.add_argument("--align", default="1,65536,2097152")
     args = ap.parse_args()
     import torch
 
@@ -97,14 +100,26 @@ def main():
     emit("h2d_2s", timed(h2d(2)))
     emit("d2h_2s", timed(d2h(2)))
 
-    pipe = HostPipeline(dev)
     pairs = list(zip(arrays, devs))
-    for w in [int(x) for x in args.windows.split(",")]:
-        emit("copy_pipe", timed(lambda: pipe.run(pairs, n, w, lambda lo, hi, s: None)), windows=w)
-    vr = VirtualRanks((2, 2, 2) if R == 8 else (R,), device=0, nblocks_per_rank=0)
-    for w in [int(x) for x in args.windows.split(",")]:
-        emit("e2e", timed(lambda: vr.allreduce_host(arrays, mode="local", windows=w)), windows=w)
-    vr.close()
+    vr = VirtualRanks((2, 2, 2) if R == 8 else (R,), device=0, nblocks_per_rank=0) if R > 1 else None
+    red = lambda lo, hi, s: vr.collective(devs, mode="local", stream=s, window=(lo, hi))  # noqa: E731
+    for lanes in [int(x) for x in args.lanes.split(",")]:
+        pipe = HostPipeline(dev, lanes=lanes)
+        for w in [int(x) for x in args.windows.split(",")]:
+            for taper in (True, False):
+                for al in [int(x) for x in args.align.split(",")]:
+                    if taper and w < 6:
+                        continue
+                    emit("copy_pipe", timed(lambda: pipe.run(pairs, n, w, lambda lo, hi, s: None, taper=taper,
+                                                             align_bytes=al)),
+                         windows=w, lanes=lanes, taper=taper, align_bytes=al)
+                    if vr:
+                        emit("pipe", timed(lambda: pipe.run(pairs, n, w, red, taper=taper, align_bytes=al)),
+                             windows=w, lanes=lanes, taper=taper, align_bytes=al)
+    if vr:
+        for w in (4, 8):
+            emit("e2e", timed(lambda: vr.allreduce_host(arrays, mode="local", windows=w)), windows=w)
+        vr.close()
 
 
 if __name__ == "__main__":
