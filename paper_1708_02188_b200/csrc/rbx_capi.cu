@@ -48,12 +48,12 @@ const void* ll_kernel_i64(int maxv);
 const void* ll_kernel_bf16(int maxv);
 const void* ll_kernel_f16(int maxv);
 const void* ll_kernel_i32(int maxv);
-const void* fused_kernel_f32(int nsrc, int nlev, int maxseg);
-const void* fused_kernel_f64(int nsrc, int nlev, int maxseg);
-const void* fused_kernel_i64(int nsrc, int nlev, int maxseg);
-const void* fused_kernel_bf16(int nsrc, int nlev, int maxseg);
-const void* fused_kernel_f16(int nsrc, int nlev, int maxseg);
-const void* fused_kernel_i32(int nsrc, int nlev, int maxseg);
+const void* fused_kernel_f32(int nsrc, int nlev, int ndst, int maxseg);
+const void* fused_kernel_f64(int nsrc, int nlev, int ndst, int maxseg);
+const void* fused_kernel_i64(int nsrc, int nlev, int ndst, int maxseg);
+const void* fused_kernel_bf16(int nsrc, int nlev, int ndst, int maxseg);
+const void* fused_kernel_f16(int nsrc, int nlev, int ndst, int maxseg);
+const void* fused_kernel_i32(int nsrc, int nlev, int ndst, int maxseg);
 const void* rings_kernel_f32();
 const void* rings_kernel_f64();
 const void* rings_kernel_i64();
@@ -298,28 +298,52 @@ unsigned long long* ll_area_of(uint32_t* sig) {
   return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(sig) + ll_offset());
 }
 
-const void* fused_kernel_for(int dtype, int nsrc, int nlev, int maxseg) {
+const void* fused_kernel_for(int dtype, int nsrc, int nlev, int ndst, int maxseg) {
   switch (dtype) {
-    case RBX_F32: return rbx::fused_kernel_f32(nsrc, nlev, maxseg);
-    case RBX_F64: return rbx::fused_kernel_f64(nsrc, nlev, maxseg);
-    case RBX_I64: return rbx::fused_kernel_i64(nsrc, nlev, maxseg);
-    case RBX_BF16: return rbx::fused_kernel_bf16(nsrc, nlev, maxseg);
-    case RBX_F16: return rbx::fused_kernel_f16(nsrc, nlev, maxseg);
-    case RBX_I32: return rbx::fused_kernel_i32(nsrc, nlev, maxseg);
+    case RBX_F32: return rbx::fused_kernel_f32(nsrc, nlev, ndst, maxseg);
+    case RBX_F64: return rbx::fused_kernel_f64(nsrc, nlev, ndst, maxseg);
+    case RBX_I64: return rbx::fused_kernel_i64(nsrc, nlev, ndst, maxseg);
+    case RBX_BF16: return rbx::fused_kernel_bf16(nsrc, nlev, ndst, maxseg);
+    case RBX_F16: return rbx::fused_kernel_f16(nsrc, nlev, ndst, maxseg);
+    case RBX_I32: return rbx::fused_kernel_i32(nsrc, nlev, ndst, maxseg);
     default: return nullptr;
   }
 }
 
-// Arguments of the specialised FUSED kernel from a FUSED allreduce plan: step 0 folds
-// every segment from all N buffers and stores into all N, step 1 is the exit wait.
+// Shape of a plan the specialised FUSED kernel runs: step 0 (after the entry wait)
+// does every segment with the same (sources, nesting, destinations), step 1 is the
+// exit wait.  Allreduce: fold all N buffers, store into all N; reduce-scatter: fold
+// all N, store into mine; all-gather: copy mine into the N-1 peers.
+bool fused_shape(const rbx::Plan& p, int N, int* nsrc, int* nlev, int* ndst) {
+  if (p.nsteps != 2 || p.steps[1].nseg != 0 || p.nentry != N - 1) return false;
+  const rbx::Step& st = p.steps[0];
+  if (st.nseg < 1) return false;
+  const rbx::Seg& s0 = p.segs[st.seg0];
+  const bool fold = s0.nsrc == N && (s0.ndst == N || s0.ndst == 1);
+  const bool copy = s0.nsrc == 1 && s0.ndst == N - 1 && s0.nlev == 1;
+  if (!fold && !copy) return false;
+  for (int k = 0; k < st.nseg; ++k) {
+    const rbx::Seg& sg = p.segs[st.seg0 + k];
+    if (sg.nsrc != s0.nsrc || sg.ndst != s0.ndst || sg.acc || sg.nlev != s0.nlev) return false;
+    for (int j = 0; j < sg.nsrc; ++j)
+      if (sg.ctrl[j] != s0.ctrl[j]) return false;
+  }
+  *nsrc = s0.nsrc;
+  *nlev = s0.nlev;
+  *ndst = s0.ndst;
+  return true;
+}
+
+// Arguments of the specialised FUSED kernel from a plan of fused_shape().
 template <int MAXSEG>
 bool fused_args_from_plan(const rbx_comm* c, const rbx::Plan& p, const std::vector<void*>& table, int threads,
                           rbx::FusedArgsT<MAXSEG>* a) {
   std::memset(a, 0, sizeof(*a));
   const int N = c->nranks;
-  if (p.nsteps != 2 || p.steps[1].nseg != 0 || p.nentry != N - 1) return false;
+  int nsrc, nlev, ndst;
+  if (!fused_shape(p, N, &nsrc, &nlev, &ndst)) return false;
   const rbx::Step& st = p.steps[0];
-  if (st.nseg < 1 || st.nseg > MAXSEG) return false;
+  if (st.nseg > MAXSEG) return false;
   a->nseg = st.nseg;
   a->me = c->rank;
   a->npeers = N - 1;
@@ -331,13 +355,9 @@ bool fused_args_from_plan(const rbx_comm* c, const rbx::Plan& p, const std::vect
     a->peer_sig[i++] = c->sig[q];
   }
   const rbx::Seg& s0 = p.segs[st.seg0];
-  for (int j = 0; j < N; ++j) a->ctrl[j] = s0.ctrl[j];
-  int u = 0;
+  for (int j = 0; j < nsrc; ++j) a->ctrl[j] = s0.ctrl[j];
   for (int k = 0; k < st.nseg; ++k) {
     const rbx::Seg& sg = p.segs[st.seg0 + k];
-    if (sg.nsrc != N || sg.ndst != N || sg.acc || sg.nlev != s0.nlev) return false;
-    for (int j = 0; j < N; ++j)
-      if (sg.ctrl[j] != s0.ctrl[j]) return false;
     rbx::FusedSeg& fs = a->seg[k];
     fs.vec_begin = sg.vec_begin;
     fs.nvec = sg.nvec;
@@ -345,12 +365,10 @@ bool fused_args_from_plan(const rbx_comm* c, const rbx::Plan& p, const std::vect
     fs.off = sg.off;
     fs.head = sg.head;
     fs.tail = sg.tail;
-    for (int j = 0; j < N; ++j) {
-      fs.src[j] = static_cast<const char*>(table[sg.tbl + sg.src[j]]);
-      fs.dst[j] = static_cast<char*>(table[sg.tbl + sg.dst[j]]);
-    }
+    for (int j = 0; j < nsrc; ++j) fs.src[j] = static_cast<const char*>(table[sg.tbl + sg.src[j]]);
+    for (int j = 0; j < ndst; ++j) fs.dst[j] = static_cast<char*>(table[sg.tbl + sg.dst[j]]);
   }
-  u = RBX_FUSED_LD / N > 0 ? RBX_FUSED_LD / N : 1;
+  const int u = RBX_FUSED_LD / nsrc > 0 ? RBX_FUSED_LD / nsrc : 1;
   a->tile = threads * u;
   return true;
 }
@@ -504,9 +522,10 @@ int set_carveouts(int device, int pct) {
     fns.push_back(kernel_for(dt));
     fns.push_back(ll_kernel_for(dt, 1));
     fns.push_back(ll_kernel_for(dt, RBX_MAX_RANKS));
-    for (int n : {2, 4, 8})
+    for (int n : {1, 2, 4, 8})
       for (int l = 1; l <= 3; ++l)
-        for (int ms : {1, RBX_FUSED_MAXSEG}) fns.push_back(fused_kernel_for(dt, n, l, ms));
+        for (int d : {1, 3, 7, n})
+          for (int ms : {1, RBX_FUSED_MAXSEG}) fns.push_back(fused_kernel_for(dt, n, l, d, ms));
     for (int v : {2, 4, 8})
       for (int l = 1; l <= 3; ++l) fns.push_back(local_kernel_for(dt, v, l));
     fns.push_back(rings_kernel_for(dt));
@@ -1052,12 +1071,16 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
     // RING_DIMS over a one-dimensional grid is the same single ring fold as FUSED (same
     // order, same pushes): both go through the specialised kernel
     const bool one_ring = mode == RBX_MODE_RING_DIMS && c->geo.active_dims().size() == 1;
-    const bool fused = (mode == RBX_MODE_FUSED || mode == RBX_MODE_AUTO || one_ring) && op == RBX_OP_ALLREDUCE &&
-                       !push && !ws;
-    if (fused && c->fused_specialised) {
-      const int nseg = host[0].nsteps ? host[0].steps[0].nseg : 0;
+    // reduce-scatter / all-gather alone: the same kernel with one destination / one source
+    const bool fused = ((mode == RBX_MODE_FUSED || mode == RBX_MODE_AUTO || one_ring) && op == RBX_OP_ALLREDUCE &&
+                        !push && !ws) ||
+                       ((mode == RBX_MODE_FUSED || mode == RBX_MODE_AUTO) &&
+                        (op == RBX_OP_REDUCE_SCATTER || op == RBX_OP_ALLGATHER) && !ws);
+    int f_nsrc = 0, f_nlev = 0, f_ndst = 0;
+    if (fused && c->fused_specialised && fused_shape(host[0], c->nranks, &f_nsrc, &f_nlev, &f_ndst)) {
+      const int nseg = host[0].steps[0].nseg;
       const int maxseg = nseg <= 1 ? 1 : RBX_FUSED_MAXSEG;
-      const void* fn = fused_kernel_for(dtype, c->nranks, (int)c->geo.active_dims().size(), maxseg);
+      const void* fn = fused_kernel_for(dtype, f_nsrc, f_nlev, f_ndst, maxseg);
       int per_sm = 0;
       if (fn) RBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, c->threads, 0));
       if (fn && per_sm * c->sm_count >= c->nblocks) {
@@ -1414,7 +1437,7 @@ int rbx_fused_harness(const int* dims, int ndims, int rank, void* const* bufs, s
   spec.vec = 16 / es;
   spec.mis = misalign(table, es);
   if (!rbx::build_plan(tmp.geo, rank, (int64_t)count, spec, 0, plan.get(), true, &err)) return fail(RBX_ERR_INVALID, err);
-  const void* fn = fused_kernel_for(dtype, tmp.nranks, (int)tmp.geo.active_dims().size(), 1);
+  const void* fn = fused_kernel_for(dtype, tmp.nranks, (int)tmp.geo.active_dims().size(), tmp.nranks, 1);
   if (!fn) return fail(RBX_ERR_UNSUPPORTED, "no specialised fused kernel for this grid");
   rbx::FusedArgsT<1> a;
   if (!fused_args_from_plan(&tmp, *plan, table, tmp.threads, &a)) return fail(RBX_ERR_UNSUPPORTED, "plan shape");

@@ -13,7 +13,10 @@
 //           NVLink-mapped peers), folded in registers in the reference's
 //           nested order (FoldState, rbx_kernel.cuh), the result stored with
 //           16-byte stores into all N buffers -- reduce-scatter and all-gather
-//           in one pass, bit-identical to replay();
+//           in one pass, bit-identical to replay().  The same loop with one
+//           destination (my buffer) is reduce_scatter alone (runtime.py:
+//           278-284); with one source (my region) and the N-1 peers as
+//           destinations it is allgather alone (runtime.py:287-292);
 //   EXIT    st.release.sys "my pushes landed / I am done reading you" to the
 //           matched CTA of every peer, then wait for theirs.
 //
@@ -65,8 +68,9 @@ struct FusedArgsT {
 
 // One pass of U vectors per thread starting at step vector `lo`: all NSRC x U
 // loads first, then the folds, then NDST x U stores.  FULL: every vector is in
-// range and in segment `s0` (no predicates, no segment search).
-template <typename T, int NSRC, int NLEV, int U, bool FULL, int MAXSEG>
+// range and in segment `s0` (no predicates, no segment search).  NSRC == 1 is a
+// copy (the all-gather half): the loaded bits are stored as they are.
+template <typename T, int NSRC, int NLEV, int NDST, int U, bool FULL, int MAXSEG>
 __device__ __forceinline__ void fused_pass(const FusedArgsT<MAXSEG>& a, int s0, int64_t lo) {
   constexpr int VEC = Traits<T>::VEC;
   int4 raw[U][NSRC];
@@ -97,19 +101,24 @@ __device__ __forceinline__ void fused_pass(const FusedArgsT<MAXSEG>& a, int s0, 
   }
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    FoldState<T, VEC, NLEV> st;
+    int4 packed;
+    if constexpr (NSRC == 1) {
+      packed = raw[u][0];
+    } else {
+      FoldState<T, VEC, NLEV> st;
 #pragma unroll
-    for (int j = 0; j < NSRC; ++j) {
-      typename Traits<T>::Acc x[VEC];
+      for (int j = 0; j < NSRC; ++j) {
+        typename Traits<T>::Acc x[VEC];
 #pragma unroll
-      for (int l = 0; l < VEC; ++l) x[l] = Traits<T>::lane(raw[u][j], l);
-      st.feed(a.ctrl[j], x);
+        for (int l = 0; l < VEC; ++l) x[l] = Traits<T>::lane(raw[u][j], l);
+        st.feed(a.ctrl[j], x);
+      }
+      packed = pack_result(st);
     }
     if (ok[u]) {
-      const int4 packed = pack_result(st);
       const FusedSeg& sg = a.seg[seg[u]];
 #pragma unroll
-      for (int d = 0; d < NSRC; ++d) __stcg(reinterpret_cast<int4*>(sg.dst[d] + byte[u]), packed);
+      for (int d = 0; d < NDST; ++d) __stcg(reinterpret_cast<int4*>(sg.dst[d] + byte[u]), packed);
     }
   }
 }
@@ -129,21 +138,26 @@ __device__ __forceinline__ bool fused_spin(const uint32_t* f, uint32_t e, volati
   return true;
 }
 
-// one element of a misaligned region edge, same fold
-template <typename T, int NSRC, int NLEV, int MAXSEG>
+// one element of a misaligned region edge, same fold (a copy when NSRC == 1)
+template <typename T, int NSRC, int NLEV, int NDST, int MAXSEG>
 __device__ __forceinline__ void fused_scalar(const FusedArgsT<MAXSEG>& a, const FusedSeg& sg, int64_t elem) {
   using Tr = Traits<T>;
   using Bt = typename Tr::Bits;
   const int64_t byte = elem * (int64_t)sizeof(T);
-  FoldState<T, 1, NLEV> st;
+  Bt out;
+  if constexpr (NSRC == 1) {
+    out = __ldcg(reinterpret_cast<const Bt*>(sg.src[0] + byte));
+  } else {
+    FoldState<T, 1, NLEV> st;
 #pragma unroll
-  for (int j = 0; j < NSRC; ++j) {
-    typename Tr::Acc x[1] = {Tr::from_bits(__ldcg(reinterpret_cast<const Bt*>(sg.src[j] + byte)))};
-    st.feed(a.ctrl[j], x);
+    for (int j = 0; j < NSRC; ++j) {
+      typename Tr::Acc x[1] = {Tr::from_bits(__ldcg(reinterpret_cast<const Bt*>(sg.src[j] + byte)))};
+      st.feed(a.ctrl[j], x);
+    }
+    out = Tr::to_bits(st.result(0));
   }
-  const Bt out = Tr::to_bits(st.result(0));
 #pragma unroll
-  for (int d = 0; d < NSRC; ++d) __stcg(reinterpret_cast<Bt*>(sg.dst[d] + byte), out);
+  for (int d = 0; d < NDST; ++d) __stcg(reinterpret_cast<Bt*>(sg.dst[d] + byte), out);
 }
 
 // vectors per thread per pass for a fold of NSRC operands
@@ -152,7 +166,7 @@ __host__ __device__ constexpr int fused_unroll() {
   return RBX_FUSED_LD / NSRC > 0 ? RBX_FUSED_LD / NSRC : 1;
 }
 
-template <typename T, int NSRC, int NLEV, int MAXSEG>
+template <typename T, int NSRC, int NLEV, int NDST, int MAXSEG>
 __global__ void __launch_bounds__(512, 1) rbx_fused_kernel(const __grid_constant__ FusedArgsT<MAXSEG> a) {
   constexpr int U = fused_unroll<NSRC>();
   const int b = blockIdx.x, nb = gridDim.x;
@@ -217,9 +231,9 @@ __global__ void __launch_bounds__(512, 1) rbx_fused_kernel(const __grid_constant
     const bool full_tile = lo + tile <= a.total_vec && (MAXSEG == 1 || lo + tile <= sg.vec_begin + sg.nvec);
     for (int64_t p = lo; p < lo + tile; p += (int64_t)U * blockDim.x) {
       if (full_tile)
-        fused_pass<T, NSRC, NLEV, U, true, MAXSEG>(a, s_cur, p);
+        fused_pass<T, NSRC, NLEV, NDST, U, true, MAXSEG>(a, s_cur, p);
       else
-        fused_pass<T, NSRC, NLEV, U, false, MAXSEG>(a, s_cur, p);
+        fused_pass<T, NSRC, NLEV, NDST, U, false, MAXSEG>(a, s_cur, p);
     }
     if (ntiles <= nb) break;  // one tile per CTA, no counter
     if (a.dbg & 16) {         // A/B: static round-robin ownership (CTA b: tiles b, b+nb, ...)
@@ -236,7 +250,7 @@ __global__ void __launch_bounds__(512, 1) rbx_fused_kernel(const __grid_constant
   for (int k = b % nb; k < a.nseg; k += nb) {
     const FusedSeg& sg = a.seg[k];
     for (int i = threadIdx.x; i < sg.head + sg.tail; i += blockDim.x)
-      fused_scalar<T, NSRC, NLEV, MAXSEG>(
+      fused_scalar<T, NSRC, NLEV, NDST, MAXSEG>(
           a, sg, i < sg.head ? sg.off + i : sg.body_off + sg.nvec * Traits<T>::VEC + (i - sg.head));
   }
   if (tr) tr[4] = global_ns();
@@ -279,9 +293,13 @@ __global__ void __launch_bounds__(512, 1) rbx_fused_kernel(const __grid_constant
   if (tr) tr[31] = global_ns();
 }
 
-// (operand count, nesting depth) of the grids with a specialised kernel: every
-// factorization of the B200 box's 2, 4 and 8 GPUs.
-#define RBX_FUSED_SHAPES(X) X(2, 1) X(4, 1) X(4, 2) X(8, 1) X(8, 2) X(8, 3)
+// (operand count, nesting depth, destinations) with a specialised kernel, for
+// every factorization of the B200 box's 2, 4 and 8 GPUs: allreduce (fold N,
+// store N), reduce-scatter (fold N, store 1), all-gather (copy 1, store N-1).
+#define RBX_FUSED_SHAPES(X)                                                                    \
+  X(2, 1, 2) X(4, 1, 4) X(4, 2, 4) X(8, 1, 8) X(8, 2, 8) X(8, 3, 8)                            \
+  X(2, 1, 1) X(4, 1, 1) X(4, 2, 1) X(8, 1, 1) X(8, 2, 1) X(8, 3, 1)                            \
+  X(1, 1, 1) X(1, 1, 3) X(1, 1, 7)
 #define RBX_FUSED_MAXSEG 16
 
 }  // namespace rbx

@@ -4,11 +4,11 @@
 #include "rbx_rings.cuh"
 
 namespace rbx {
-const void* fused_kernel_f64(int nsrc, int nlev, int maxseg) {
-#define RBX_FUSED_CASE(N, L)                                                                          \
-  if (nsrc == N && nlev == L)                                                                         \
-    return maxseg == 1 ? reinterpret_cast<const void*>(&rbx_fused_kernel<double, N, L, 1>)                \
-                       : reinterpret_cast<const void*>(&rbx_fused_kernel<double, N, L, RBX_FUSED_MAXSEG>);
+const void* fused_kernel_f64(int nsrc, int nlev, int ndst, int maxseg) {
+#define RBX_FUSED_CASE(N, L, D)                                                                                        \
+  if (nsrc == N && nlev == L && ndst == D)                                                                             \
+    return maxseg == 1 ? reinterpret_cast<const void*>(&rbx_fused_kernel<double, N, L, D, 1>)                          \
+                       : reinterpret_cast<const void*>(&rbx_fused_kernel<double, N, L, D, RBX_FUSED_MAXSEG>);
   RBX_FUSED_SHAPES(RBX_FUSED_CASE)
 #undef RBX_FUSED_CASE
   return nullptr;

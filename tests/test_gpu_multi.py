@@ -137,14 +137,19 @@ def test_reference_runtime_digests_and_traffic(world):
 def test_reduce_scatter_allgather_pair(world):
     if cuda_count() < 1:
         pytest.skip("no CUDA device")
+    # fused / auto: reduce_scatter and allgather each through the specialised kernel
+    # (fold N -> store 1, copy 1 -> store N-1), aligned bodies and scalar edges
     cases = [{"dims": d, "mode": m, "dtype": "f32", "lengths": [10007, 1], "seed": 11, "op": "rs+ag"}
              for d in _dims_for(world) for m in ("fused", "ring_dims", "push")]
+    cases += [{"dims": d, "mode": "auto", "dtype": dt, "lengths": [1_000_003, 4096], "seed": 12, "op": "rs+ag"}
+              for d in _dims_for(world) for dt in ("f32", "f64", "i64")]
     res = _spawn(world, cases)
     for r in range(world):
         for dims, mode, dtype, it, length, op, dig, _ in res[r][2]:
-            parts = [orc.generate_input(11, it, q, length, "f32") for q in range(world)]
+            seed = 11 if mode != "auto" else 12
+            parts = [orc.generate_input(seed, it, q, length, dtype) for q in range(world)]
             want = orc.closed_form_allreduce(orc.Grid(dims), parts)
-            assert dig == orc.sha256(want), (dims, mode, length)
+            assert dig == orc.sha256(want), (dims, mode, dtype, length)
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])
