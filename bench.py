@@ -67,7 +67,7 @@ def parse_args():
                         "host PCIe ceiling, profiles/r02_e2e_probe_align_1gpu.jsonl); N>1 uses the runtime's default")
     a = p.parse_args()
     if a.e2e_chunks is None:
-        a.e2e_chunks = 12 if a.gpus == 1 else 32
+        a.e2e_chunks = 12 if a.gpus == 1 else None  # N>1: hoststage.default_windows
     return a
 
 

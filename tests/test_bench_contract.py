@@ -53,10 +53,10 @@ def test_busbw_and_workload_names():
 def test_default_arguments(monkeypatch):
     monkeypatch.setattr(sys, "argv", ["bench.py"])
     a = bench.parse_args()
-    assert (a.gpus, a.steps, a.warmup, a.impl, a.elems, a.e2e_chunks) == (1, 20, 5, "ours", bench.N_ELEM, 8)
+    assert (a.gpus, a.steps, a.warmup, a.impl, a.elems, a.e2e_chunks) == (1, 20, 5, "ours", bench.N_ELEM, 12)
     assert a.warmup >= 3  # timing rules: W >= 3
     monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4"])
-    assert bench.parse_args().e2e_chunks == 32
+    assert bench.parse_args().e2e_chunks is None  # N>1: the runtime's default windows
 
 
 def test_gpus_n_without_torchrun_self_launches(monkeypatch):
