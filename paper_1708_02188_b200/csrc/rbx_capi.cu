@@ -336,7 +336,7 @@ bool fused_shape(const rbx::Plan& p, int N, int* nsrc, int* nlev, int* ndst) {
 
 // Arguments of the specialised FUSED kernel from a plan of fused_shape().
 template <int MAXSEG>
-bool fused_args_from_plan(const rbx_comm* c, const rbx::Plan& p, const std::vector<void*>& table, int threads,
+bool fused_args_from_plan(const rbx_comm* c, const rbx::Plan& p, const std::vector<void*>& table,
                           rbx::FusedArgsT<MAXSEG>* a) {
   std::memset(a, 0, sizeof(*a));
   const int N = c->nranks;
@@ -368,8 +368,6 @@ bool fused_args_from_plan(const rbx_comm* c, const rbx::Plan& p, const std::vect
     for (int j = 0; j < nsrc; ++j) fs.src[j] = static_cast<const char*>(table[sg.tbl + sg.src[j]]);
     for (int j = 0; j < ndst; ++j) fs.dst[j] = static_cast<char*>(table[sg.tbl + sg.dst[j]]);
   }
-  const int u = RBX_FUSED_LD / nsrc > 0 ? RBX_FUSED_LD / nsrc : 1;
-  a->tile = threads * u;
   return true;
 }
 
@@ -1087,11 +1085,11 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
         bool ok;
         if (maxseg == 1) {
           cp.fused1 = std::make_shared<rbx::FusedArgsT<1>>();
-          ok = fused_args_from_plan(c, host[0], ptrs, c->threads, cp.fused1.get());
+          ok = fused_args_from_plan(c, host[0], ptrs, cp.fused1.get());
           if (!ok) cp.fused1.reset();
         } else {
           cp.fusedN = std::make_shared<rbx::FusedArgsT<RBX_FUSED_MAXSEG>>();
-          ok = fused_args_from_plan(c, host[0], ptrs, c->threads, cp.fusedN.get());
+          ok = fused_args_from_plan(c, host[0], ptrs, cp.fusedN.get());
           if (!ok) cp.fusedN.reset();
         }
         if (ok) cp.fused_fn = fn;
@@ -1440,7 +1438,7 @@ int rbx_fused_harness(const int* dims, int ndims, int rank, void* const* bufs, s
   const void* fn = fused_kernel_for(dtype, tmp.nranks, (int)tmp.geo.active_dims().size(), tmp.nranks, 1);
   if (!fn) return fail(RBX_ERR_UNSUPPORTED, "no specialised fused kernel for this grid");
   rbx::FusedArgsT<1> a;
-  if (!fused_args_from_plan(&tmp, *plan, table, tmp.threads, &a)) return fail(RBX_ERR_UNSUPPORTED, "plan shape");
+  if (!fused_args_from_plan(&tmp, *plan, table, &a)) return fail(RBX_ERR_UNSUPPORTED, "plan shape");
   a.timeout_ns = 1000000000ull;
   a.err = errs[dev];
   a.trace = nullptr;

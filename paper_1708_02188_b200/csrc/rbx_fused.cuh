@@ -50,7 +50,6 @@ template <int MAXSEG>
 struct FusedArgsT {
   int nseg, me, npeers;
   int64_t total_vec;
-  int tile;                           // vectors per work tile (one pass: threads x U)
   uint32_t* my_sig;
   uint32_t* peer_sig[RBX_MAX_RANKS];  // signal areas of the peers (mapped), in peer_rank order
   uint8_t peer_rank[RBX_MAX_RANKS];
@@ -160,15 +159,21 @@ __device__ __forceinline__ void fused_scalar(const FusedArgsT<MAXSEG>& a, const 
   for (int d = 0; d < NDST; ++d) __stcg(reinterpret_cast<Bt*>(sg.dst[d] + byte), out);
 }
 
-// vectors per thread per pass for a fold of NSRC operands
-template <int NSRC>
-__host__ __device__ constexpr int fused_unroll() {
-  return RBX_FUSED_LD / NSRC > 0 ? RBX_FUSED_LD / NSRC : 1;
+#ifndef RBX_FUSED_RS_LD
+#define RBX_FUSED_RS_LD 16  // the same for reduce-scatter alone (loads only, one local store)
+#endif
+
+// vectors per thread per pass for a fold of nsrc operands into ndst buffers (the
+// deeper reduce-scatter pass spills the 64-bit accumulators of 8-byte types)
+template <typename T>
+__host__ __device__ constexpr int fused_unroll(int nsrc, int ndst) {
+  const int ld = (ndst == 1 && nsrc > 1 && sizeof(T) < 8) ? RBX_FUSED_RS_LD : RBX_FUSED_LD;
+  return ld / nsrc > 0 ? ld / nsrc : 1;
 }
 
 template <typename T, int NSRC, int NLEV, int NDST, int MAXSEG>
 __global__ void __launch_bounds__(512, 1) rbx_fused_kernel(const __grid_constant__ FusedArgsT<MAXSEG> a) {
-  constexpr int U = fused_unroll<NSRC>();
+  constexpr int U = fused_unroll<T>(NSRC, NDST);
   const int b = blockIdx.x, nb = gridDim.x;
   __shared__ uint32_t s_epoch;
   __shared__ int s_fail, s_next;
@@ -216,7 +221,7 @@ __global__ void __launch_bounds__(512, 1) rbx_fused_kernel(const __grid_constant
 
   // FOLD: tile t = vectors [t*tile, (t+1)*tile); CTA b starts with tile b, then claims
   // nb, nb+1, ... from the per-launch counter (claim issued before the tile's loads)
-  const int64_t tile = a.tile;
+  const int64_t tile = (int64_t)U * blockDim.x;  // one pass of the block
   const int64_t ntiles = (a.total_vec + tile - 1) / tile;
   const int64_t tlimit = a.fault_milli < 0 ? ntiles : ntiles * a.fault_milli / 1000;
   unsigned int* ctr = reinterpret_cast<unsigned int*>(my_sig + SigLayout::tiles_off);
