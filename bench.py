@@ -674,7 +674,8 @@ def main_multi(args):
                          f"host has {cores} cores"}
     dist.barrier()
 
-    traffic = ncu_traffic("nvlink_tx_2_25.6M_f32") if (world == 2 and n == N_ELEM and args.dtype == "f32") else None
+    traffic_key = {2: "nvlink_tx_2_25.6M_f32", 4: "nvlink_tx_2x2_25.6M_f32"}.get(world)
+    traffic = ncu_traffic(traffic_key) if (traffic_key and n == N_ELEM and args.dtype == "f32") else None
     if rank == 0:
         # peak: the recipe's measured NVLink figure (B200_PROFILING.md: 770 GB/s peer copy per direction).
         # The copy-engine ceiling measured in this run is reported beside it, not used: with more than
@@ -700,7 +701,7 @@ def main_multi(args):
             "roofline": {"bound": "nvlink", "achieved": round(bw, 2), "peak": peak, "unit": "GB/s",
                          "frac": round(bw / peak, 4), "traffic": traffic,
                          "traffic_kind": "NVLink TX bytes per launch per GPU (ncu nvltx__bytes.sum, user + protocol; "
-                                         "2-GPU harness, profiles/ncu_traffic.json)" if traffic else None,
+                                         f"{world}-GPU harness, profiles/ncu_traffic.json)" if traffic else None,
                          "peak_source": peak_src, "ceiling": ceiling,
                          "frac_of_770": round(bw / MEASURED_PEER_GBS, 4), "frac_of_900": round(bw / NOMINAL_NVLINK_GBS, 4),
                          "algorithmic_bytes_per_launch": int(2 * (world - 1) / world * nbytes)},
