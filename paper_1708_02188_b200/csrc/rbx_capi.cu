@@ -1098,7 +1098,8 @@ int real_collective(rbx_comm* c, void* const* bufs, const size_t* counts, int nb
     // the paper's per-dimension rings through the specialised kernel: whole aligned buffer,
     // 4/8-byte types (16-bit types keep fp32 stage partials in workspaces: generic kernel)
     const bool matched_stages = (mode == RBX_MODE_RING_DIMS && !one_ring && !ws) || (push && c->push_specialised);
-    if (matched_stages && op == RBX_OP_ALLREDUCE && nbufs == 1 && whole && spec.mis == 0 && c->rings_specialised) {
+    if (matched_stages && (op == RBX_OP_ALLREDUCE || op == RBX_OP_REDUCE_SCATTER) && nbufs == 1 && whole &&
+        spec.mis == 0 && c->rings_specialised) {
       const void* fn = rings_kernel_for(dtype);
       int per_sm = 0;
       if (fn) RBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, c->threads, 0));

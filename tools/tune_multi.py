@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--elems", default="25600000")
     ap.add_argument("--dims", default=None)
     ap.add_argument("--modes", default="fused,fused_pull,ring_dims")
+    ap.add_argument("--ops", default="allreduce", help="allreduce,reduce_scatter,allgather")
     ap.add_argument("--nblocks", default="148,296")
     ap.add_argument("--threads", default="256,512")
     ap.add_argument("--iters", type=int, default=20)
@@ -43,30 +44,33 @@ def main():
             for n in [int(x) for x in args.elems.split(",")]:
                 work = ctx.empty(n, "f32")
                 work.normal_()
-                for mode in args.modes.split(","):
-                    ts = []
-                    for it in range(args.iters + 3):
-                        if args.flush:
-                            scratch.fill_(1.0)
-                            scratch.sum()
-                        torch.cuda._sleep(100_000)
-                        ctx.barrier()
-                        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                        s.record(stream)
-                        ctx.collective("allreduce", work, mode=mode)
-                        e.record(stream)
-                        torch.cuda.synchronize()
-                        if it >= 3:
-                            ts.append(s.elapsed_time(e))
-                        work.mul_(0.125)
-                    ctx.check()
-                    t = torch.tensor(ts, device=dev)
-                    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                    med = t.median().item() / 1e3
-                    bw = 2 * (world - 1) / world * n * 4 / med / 1e9
-                    if rank == 0:
-                        print(f"mode={mode:10s} nb={ctx.nblocks:4d}(req {nb:4d}) th={th:4d} n={n:10d} "
-                              f"t={med * 1e6:9.1f}us busbw={bw:7.1f} GB/s", flush=True)
+                for op in args.ops.split(","):
+                    for mode in args.modes.split(","):
+                        ts = []
+                        for it in range(args.iters + 3):
+                            if args.flush:
+                                scratch.fill_(1.0)
+                                scratch.sum()
+                            torch.cuda._sleep(100_000)
+                            ctx.barrier()
+                            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                            s.record(stream)
+                            ctx.collective(op, work, mode=mode)
+                            e.record(stream)
+                            torch.cuda.synchronize()
+                            if it >= 3:
+                                ts.append(s.elapsed_time(e))
+                            work.mul_(0.125)
+                        ctx.check()
+                        t = torch.tensor(ts, device=dev)
+                        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                        med = t.median().item() / 1e3
+                        # bus bytes: 2(N-1)/N S for allreduce, (N-1)/N S for either half alone
+                        f = 2 if op == "allreduce" else 1
+                        bw = f * (world - 1) / world * n * 4 / med / 1e9
+                        if rank == 0:
+                            print(f"op={op:14s} mode={mode:10s} nb={ctx.nblocks:4d}(req {nb:4d}) th={th:4d} n={n:10d} "
+                                  f"t={med * 1e6:9.1f}us busbw={bw:7.1f} GB/s", flush=True)
             ctx.close()
     dist.destroy_process_group()
 
