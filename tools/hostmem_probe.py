@@ -3,7 +3,6 @@ array) vs torch's pinned allocator (cudaHostAlloc), both directions at once
 (diagnostic).  python tools/hostmem_probe.py [--mb 102.4] [--bufs 8]"""
 
 import argparse
-import ctypes
 import json
 import os
 import statistics
