@@ -164,16 +164,19 @@ __device__ __forceinline__ void fused_scalar(const FusedArgsT<MAXSEG>& a, const 
 #endif
 
 // vectors per thread per pass for a fold of nsrc operands into ndst buffers (the
-// deeper reduce-scatter pass spills the 64-bit accumulators of 8-byte types)
+// deeper reduce-scatter pass spills the 64-bit accumulators of 8-byte types; the
+// 7-destination copy of a bucket list spills its segment bookkeeping at 8)
 template <typename T>
-__host__ __device__ constexpr int fused_unroll(int nsrc, int ndst) {
-  const int ld = (ndst == 1 && nsrc > 1 && sizeof(T) < 8) ? RBX_FUSED_RS_LD : RBX_FUSED_LD;
+__host__ __device__ constexpr int fused_unroll(int nsrc, int ndst, int maxseg) {
+  const int ld = (ndst == 1 && nsrc > 1 && sizeof(T) < 8) ? RBX_FUSED_RS_LD
+                 : (nsrc == 1 && ndst >= 7 && maxseg > 1) ? RBX_FUSED_LD / 2
+                                                          : RBX_FUSED_LD;
   return ld / nsrc > 0 ? ld / nsrc : 1;
 }
 
 template <typename T, int NSRC, int NLEV, int NDST, int MAXSEG>
 __global__ void __launch_bounds__(512, 1) rbx_fused_kernel(const __grid_constant__ FusedArgsT<MAXSEG> a) {
-  constexpr int U = fused_unroll<T>(NSRC, NDST);
+  constexpr int U = fused_unroll<T>(NSRC, NDST, MAXSEG);
   const int b = blockIdx.x, nb = gridDim.x;
   __shared__ uint32_t s_epoch;
   __shared__ int s_fail, s_next;

@@ -211,14 +211,18 @@ __device__ __forceinline__ void ll_fold_unit(const LLRank& R, const uint8_t* ord
       f.feed(R.ctrl[k], x);
     }
   }
+  // the result sits at level nlev-1; carry it up to the top level with selects on
+  // static indices (picking f.a[nlev-1] directly made ptxas index a local-memory
+  // copy of the accumulators for 2-lane units)
+#pragma unroll
+  for (int L = 1; L < RBX_MAX_LEVELS; ++L) {
+    const bool above = L >= nlev;
+#pragma unroll
+    for (int l = 0; l < LPU; ++l) f.a[L][l] = above ? f.a[L - 1][l] : f.a[L][l];
+  }
   Acc r[LPU];
 #pragma unroll
-  for (int l = 0; l < LPU; ++l) {
-    r[l] = f.a[0][l];
-#pragma unroll
-    for (int L = 1; L < RBX_MAX_LEVELS; ++L)
-      if (L == nlev - 1) r[l] = f.a[L][l];
-  }
+  for (int l = 0; l < LPU; ++l) r[l] = f.a[RBX_MAX_LEVELS - 1][l];
   F::pack(r, res);
 }
 
