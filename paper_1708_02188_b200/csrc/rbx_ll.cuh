@@ -235,7 +235,6 @@ __global__ void __launch_bounds__(512, 1) rbx_ll_kernel(const __grid_constant__ 
   const LLRank& R = a.rank[v];
   const int N = a.nranks, me = R.me;
   const int64_t cap = a.cap;
-  __shared__ uint32_t s_epoch;
   __shared__ int s_fail, s_peer;
   pdl_wait();  // before any memory access (programmatic dependent launch)
   // timeline of thread 0 of the first and last CTA of the first hosted rank:
@@ -247,14 +246,17 @@ __global__ void __launch_bounds__(512, 1) rbx_ll_kernel(const __grid_constant__ 
     tr[0] = global_ns();
   }
   if (threadIdx.x == 0) {
-    s_epoch = *(volatile uint32_t*)(R.my_sig + SigLayout::epoch_off) + 1u;
     s_fail = 0;
     s_peer = -1;
   }
   __syncthreads();
   pdl_launch_dependents();
   if (a.fault == 0) return;  // injected crash before any data moved
-  LLWait wt{s_epoch, global_ns(), a.timeout_ns, (volatile uint32_t*)(R.my_sig + SigLayout::abort_off), false, -1};
+  // every thread reads the epoch itself (one broadcast load, no barrier behind it), so
+  // its latency overlaps the first data loads instead of preceding them.  It cannot
+  // change during this launch: the last CTA to finish publishes the next one.
+  const uint32_t e0 = *(volatile uint32_t*)(R.my_sig + SigLayout::epoch_off) + 1u;
+  LLWait wt{e0, global_ns(), a.timeout_ns, (volatile uint32_t*)(R.my_sig + SigLayout::abort_off), false, -1};
   if (tr) tr[1] = global_ns();
   const uint32_t e = wt.e;
   const int64_t tid = (int64_t)b * blockDim.x + threadIdx.x, nthr = (int64_t)a.nb * blockDim.x;
