@@ -75,3 +75,19 @@ def test_pipeline_lanes_cover_every_window_once(nbuf, lanes):
             d += 1
     for t in hosts + devs:
         assert torch.equal(t, torch.ones(n, dtype=torch.int32))  # every element in exactly one piece
+
+
+@pytest.mark.parametrize("n,w,align", [(25_600_000, 12, 16384), (25_600_000, 16, 16384), (102_400_000, 16, 16384),
+                                       (1_000_003, 5, 16384), (1000, 8, 16384), (5, 3, 4)])
+def test_window_bounds_aligned_edges(n, w, align):
+    """hoststage.HostPipeline rounds inner window edges to 64 KB (16384 fp32 elements):
+    copies that start off such a boundary ran slower (profiles/r02_e2e_probe_align_1gpu.jsonl)."""
+    b = window_bounds(n, w, taper=False, align=align)
+    assert b[0][0] == 0 and b[-1][1] == n
+    assert all(x[1] == y[0] for x, y in zip(b, b[1:]))
+    assert all(hi > lo for lo, hi in b)
+    assert all(lo % align == 0 for lo, _ in b)  # every window starts on the grid; only the last may end off it
+    if n >= w * align:
+        assert len(b) == w
+        sizes = [hi - lo for lo, hi in b]
+        assert max(sizes) - min(sizes) <= align + 1  # equal windows up to the rounding
