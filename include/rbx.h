@@ -110,6 +110,15 @@ int rbx_comm_inject_fault(rbx_comm_t *comm, double fraction);
  * last (32..63) CTA: 0 start, 1 plan staged, 2 entry signalled, 3+3s/4+3s/5+3s step s waited/worked/
  * signalled, 30 steps done, 31 exit.  Tracing / profiling subsystem. */
 int rbx_comm_trace(rbx_comm_t *comm, uint64_t *out, int cap);
+/* Which kernel ran this communicator's last collective (RBX_KERNEL_*): the evidence that a call took a
+ * specialised path and not the generic step interpreter. */
+#define RBX_KERNEL_NONE 0
+#define RBX_KERNEL_STEP 1   /* rbx_step_kernel: the generic step-table interpreter */
+#define RBX_KERNEL_FUSED 2  /* rbx_fused_kernel: FUSED allreduce / reduce-scatter / all-gather */
+#define RBX_KERNEL_RINGS 3  /* rbx_rings_kernel: RING_DIMS / PUSH with per-CTA matched stages */
+#define RBX_KERNEL_LL 4     /* rbx_ll_kernel: small messages, {data, epoch} words */
+#define RBX_KERNEL_LOCAL 5  /* rbx_local_kernel: all ranks on one GPU (MODE_LOCAL) */
+int rbx_comm_last_kernel(rbx_comm_t *comm, int *kind);
 /* Page-lock host memory in place (PlacedBuffer(numpy) staging, hoststage.py): copies from / to it then
  * run at the host link's DMA rate.  Memory that is already page-locked is not an error; *registered
  * (optional) is 1 only if this call registered it (then rbx_host_unregister releases it). */

@@ -74,6 +74,7 @@ def lib() -> ctypes.CDLL:
     _sig(L.rbx_comm_set_timeout, c_int, _VP, ctypes.c_double)
     _sig(L.rbx_comm_info, c_int, _VP, _INTP, _INTP, _INTP, _INTP, ctypes.POINTER(ctypes.c_uint64))
     _sig(L.rbx_comm_trace, c_int, _VP, ctypes.POINTER(ctypes.c_uint64), c_int)
+    _sig(L.rbx_comm_last_kernel, c_int, _VP, ctypes.POINTER(c_int))
     _sig(L.rbx_comm_inject_fault, c_int, _VP, ctypes.c_double)
     _sig(L.rbx_stamp, c_int, _VP, _VP)
     _sig(L.rbx_host_register, c_int, _VP, c_size, _INTP)
@@ -103,11 +104,23 @@ EXPORTED = [
     "rbx_version", "rbx_last_error", "rbx_chunk_bounds", "rbx_owned_region", "rbx_fold_order", "rbx_plan_describe",
     "rbx_device_count", "rbx_enable_peer_access", "rbx_alloc_symmetric", "rbx_free", "rbx_export_buffer", "rbx_comm_create",
     "rbx_comm_connect", "rbx_comm_destroy", "rbx_comm_set_timeout", "rbx_comm_info", "rbx_comm_trace",
+    "rbx_comm_last_kernel",
     "rbx_comm_inject_fault", "rbx_stamp", "rbx_fused_harness", "rbx_host_register", "rbx_host_unregister",
     "rbx_register_buffer", "rbx_peer_pointer", "rbx_inbox_bytes", "rbx_set_inbox",
     "rbx_allreduce", "rbx_reduce_scatter", "rbx_allgather", "rbx_allreduce_buckets", "rbx_allreduce_window",
     "rbx_barrier", "rbx_check", "rbx_vcomm_create", "rbx_vcollective", "rbx_vcollective_window",
 ]
+
+
+# rbx_comm_last_kernel codes (include/rbx.h RBX_KERNEL_*)
+KERNELS = {0: "none", 1: "step", 2: "fused", 3: "rings", 4: "ll", 5: "local"}
+
+
+def last_kernel(comm) -> str:
+    """Which kernel ran the communicator's last collective."""
+    k = ctypes.c_int(0)
+    check(lib().rbx_comm_last_kernel(comm, ctypes.byref(k)))
+    return KERNELS.get(k.value, str(k.value))
 
 
 def check(rc: int) -> None:

@@ -206,6 +206,7 @@ struct rbx_comm {
   // env RBX_FUSED_KERNEL=0 forces the generic step interpreter
   bool fused_specialised = true;
   int pdl = 1;  // programmatic dependent launch for the fused kernel; env RBX_PDL
+  int last_kernel = RBX_KERNEL_NONE;  // rbx_comm_last_kernel
   int fused_dbg = 0;  // env RBX_FUSED_DBG: experiment knobs of the fused kernel (rbx_fused.cuh FusedArgsT::dbg)
   bool plain_launch = false;  // env RBX_PLAIN_LAUNCH=1: fused kernel through cudaLaunchKernel (no launch attributes)
   bool rings_specialised = true;  // RING_DIMS through rbx_rings_kernel where possible; env RBX_RINGS_KERNEL=0: generic
@@ -729,6 +730,7 @@ int launch(rbx_comm* c, const CachedPlan& cp, int dtype, cudaStream_t stream, bo
     RBX_CUDA(cudaLaunchKernel(fn, grid, block, params, smem, stream));
   }
   c->launches++;
+  c->last_kernel = RBX_KERNEL_STEP;
   return order_after(c, stream, capturing);
 }
 
@@ -770,6 +772,7 @@ int fused_launch(rbx_comm* c, CachedPlan& cp, cudaStream_t stream, int nb) {
   else
     RBX_CUDA(cudaLaunchKernelExC(&cfg, cp.fused_fn, params));
   c->launches++;
+  c->last_kernel = RBX_KERNEL_FUSED;
   return order_after(c, stream, capturing);
 }
 
@@ -793,6 +796,7 @@ int rings_launch(rbx_comm* c, CachedPlan& cp, cudaStream_t stream, int nb) {
   if (int rc = order_before(c, stream, &capturing)) return rc;
   RBX_CUDA(cudaLaunchKernelExC(&cfg, cp.rings_fn, params));
   c->launches++;
+  c->last_kernel = RBX_KERNEL_RINGS;
   return order_after(c, stream, capturing);
 }
 
@@ -897,6 +901,7 @@ int ll_launch(rbx_comm* c, const std::vector<int>& ranks, void* const* bufs, siz
     RBX_CUDA(cudaLaunchKernelExC(&cfg, fn, params));
   }
   c->launches++;
+  c->last_kernel = RBX_KERNEL_LL;
   return order_after(c, stream, capturing);
 }
 
@@ -1326,6 +1331,12 @@ int rbx_comm_trace(rbx_comm_t* c, uint64_t* out, int cap) {
   return RBX_OK;
 }
 
+int rbx_comm_last_kernel(rbx_comm_t* c, int* kind) {
+  if (!c || !kind) return fail(RBX_ERR_INVALID, "null argument");
+  *kind = c->last_kernel;
+  return RBX_OK;
+}
+
 int rbx_comm_info(rbx_comm_t* c, int* rank, int* nranks, int* nblocks, int* threads, uint64_t* launches) {
   if (!c) return fail(RBX_ERR_INVALID, "null communicator");
   if (rank) *rank = c->rank;
@@ -1695,6 +1706,7 @@ int rbx_vcollective_window(rbx_comm_t* c, void* const* bufs, size_t count, size_
     RBX_CUDA(cudaLaunchKernel(it->second.local_fn, dim3((unsigned)it->second.local_grid), dim3((unsigned)c->threads),
                               params, 0, (cudaStream_t)stream));
     c->launches++;
+    c->last_kernel = RBX_KERNEL_LOCAL;
     return order_after(c, (cudaStream_t)stream, capturing);
   }
   if (!local && (int64_t)nb * V > c->max_coresident)

@@ -223,6 +223,12 @@ class RankContext:
         _native.check(self._L.rbx_comm_info(self._comm, None, None, ctypes.byref(nb), None, None))
         return nb.value
 
+    def last_kernel(self) -> str:
+        """Which kernel ran this rank's last collective: "fused", "rings", "ll", "step"
+        (the generic interpreter) or "none" -- the evidence that a call took a
+        specialised path."""
+        return _native.last_kernel(self._comm)
+
     def trace(self) -> dict:
         """Kernel timeline of the last launch (needs RBX_TRACE=1 before creation):
         microseconds since the first CTA started, for the first and last CTA."""

@@ -105,6 +105,10 @@ class VirtualRanks:
         self.check()
         return arrays
 
+    def last_kernel(self) -> str:
+        """Which kernel ran the last collective ("local", "fused", "rings", "ll", "step")."""
+        return _native.last_kernel(self._comm)
+
     def check(self) -> None:
         _native.check(self._L.rbx_check(self._comm))
 

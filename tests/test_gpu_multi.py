@@ -556,3 +556,70 @@ def test_specialised_kernels_randomised(world):
                 w = parts[r].copy()
                 w[lo:hi] = want[r][lo:hi]
             assert res[r][2][k] == orc.sha256(w), (r, case)
+
+
+def _kernel_rank_main(rank, world, port, cases, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1708_02188_b200.multiring import Grid
+    from paper_1708_02188_b200.runtime import RankContext
+
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dev = rank_device(rank)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = []
+    try:
+        for dims, op, mode, dtype, n in cases:
+            ctx = RankContext(rank, Grid(tuple(dims)), device=dev, mode=mode)
+            x = orc.generate_input(5, 0, rank, n, "f32" if dtype == "bf16" else dtype)
+            t = ctx.empty(n, dtype)
+            t.copy_(torch.from_numpy(x))  # bf16: RNE of the fp32 inputs
+            ctx.collective(op, t)
+            torch.cuda.synchronize()
+            out.append(((tuple(dims), op, mode, dtype, n), ctx.last_kernel()))
+            ctx.close()
+        q.put((rank, "ok", out))
+    except Exception as exc:  # noqa: BLE001
+        q.put((rank, "error", repr(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_calls_take_the_specialised_kernels(world):
+    """rbx_comm_last_kernel: each collective of the box's grids runs the kernel the
+    design says it runs -- never a silent fallback to the
+    generic step interpreter."""
+    if cuda_count() < 1:
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+
+    big, small = 1_000_000, 1000
+    grid = (2,) if world == 2 else (2, 2)
+    cases = [(grid, "allreduce", "auto", "f32", big), (grid, "reduce_scatter", "auto", "f32", big),
+             (grid, "allgather", "auto", "f32", big), (grid, "allreduce", "auto", "f32", small),
+             (grid, "allreduce", "auto", "bf16", big), (grid, "allreduce", "push", "f32", big),
+             (grid, "allreduce", "fused_pull", "f32", big)]
+    want = ["fused", "fused", "fused", "ll", "fused", "rings", "step"]
+    if world == 4:
+        cases += [(grid, "allreduce", "ring_dims", "f32", big), (grid, "reduce_scatter", "ring_dims", "f32", big),
+                  ((4,), "allreduce", "auto", "i64", big)]
+        want += ["rings", "rings", "fused"]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_kernel_rank_main, args=(r, world, port, cases, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r = q.get(timeout=600)
+        res[r[0]] = r
+    for p in procs:
+        p.join(timeout=60)
+    for r, v in res.items():
+        assert v[1] == "ok", v
+        got = [k for _, k in v[2]]
+        assert got == want, list(zip([c for c, _ in v[2]], got, want))
