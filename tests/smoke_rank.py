@@ -28,9 +28,11 @@ def smoke_rank(rank: int, port: int, q) -> None:
         t = ctx.empty(n, "f32")
         t.copy_(torch.from_numpy(parts[rank]))
         ctx.collective("allreduce", t)
+        kernel = ctx.last_kernel()
         ok = orc.sha256(t.cpu().numpy()) == orc.sha256(orc.closed_form_allreduce(orc.Grid((2,)), parts))
+        ok = ok and kernel == "fused"  # the specialised FUSED kernel, not the interpreter
         ctx.close()
         dist.destroy_process_group()
-        q.put((rank, ok, ""))
+        q.put((rank, ok, f"(kernel {kernel})"))
     except Exception as exc:  # noqa: BLE001
         q.put((rank, False, repr(exc)))
